@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the Founsure encode hot path on B200 (BASELINE.json metric: encode throughput,
+source GB/s, % of HBM roofline).
+
+Workload: BASELINE config 4 -- 256 independent stripes of k=1024 x t=4096 B
+(1 GiB of seeded uniform bytes), precode p=16 checks of degree 3, n=1280 coded symbols with
+RSD(c=0.1, delta=0.05) -- per GPU (weak scaling: each rank encodes its own 1 GiB shard of the
+same stream; --scaling strong splits one 1 GiB file instead).  One step = one pass of the
+whole hot path (precode + LT over every stripe) = one fs_encode_stripes call.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+N > 1 runs under torchrun (one process per GPU, NCCL); the graph is generated on rank 0 and
+broadcast over NCCL, stripes are sharded with no data-path collective, the time is the max
+over ranks of the CUDA-event time of K steps.  Rank 0 prints one JSON line.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1702_07409_b200 import configs, fsb, inputs  # noqa: E402
+
+METRIC = "encode throughput, source GB/s (1/2/4/8 B200), % of HBM roofline"
+SMEM_GATHER_PEAK_GBS = 36806.0   # measured: tools/microbench/mb.cu smem_gather (profiles/microbench_r01.md)
+REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = "clocks.sm,clocks.max.sm," + ",".join("clocks_event_reasons." + r for r in REASONS)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + q, "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 2 + len(REASONS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for r, v in zip(REASONS, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(r)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _shard(args, cfg, ws, rank):
+    S_total = cfg["stripes"]
+    if args.scaling == "weak":
+        return rank * S_total, S_total          # each rank: its own full-size shard
+    a, b = rank * S_total // ws, (rank + 1) * S_total // ws
+    return a, b - a
+
+
+def _graph(cfg, ws, rank, dev):
+    """Rank 0 generates; other ranks receive the CSR over NCCL (step a2)."""
+    if ws == 1:
+        return fsb.Graph.create(cfg)
+    import torch.distributed as dist
+    if rank == 0:
+        g = fsb.Graph.create(cfg)
+        arrs = g.csr()
+        sizes = torch.tensor([len(a) for a in arrs], dtype=torch.int64, device=dev)
+    else:
+        sizes = torch.zeros(4, dtype=torch.int64, device=dev)
+    dist.broadcast(sizes, 0)
+    bufs = []
+    for i, n in enumerate(sizes.tolist()):
+        t = torch.from_numpy(arrs[i]).to(dev) if rank == 0 else torch.empty(n, dtype=torch.int32, device=dev)
+        dist.broadcast(t, 0)
+        bufs.append(t.cpu().numpy())
+    if rank == 0:
+        return g
+    return fsb.Graph.from_csr(cfg, *bufs)
+
+
+def cpu_oracle_sample(cfg, seconds, max_stripes=None):
+    """The oracle, as it stands (single-threaded C), on a bounded sample of the workload:
+    whole stripes of the config until `seconds` of CPU work (at least one)."""
+    import oracle
+    go = oracle.generate_graph(cfg)
+    S = cfg["stripes"] if max_stripes is None else max_stripes
+    done, t_enc = 0, 0.0
+    while done < S and (t_enc < seconds or done == 0):
+        D = inputs.stripe_data(cfg, stripe_begin=done, num_stripes=1).numpy()
+        t0 = time.perf_counter()
+        oracle.encode(go, D[0])
+        t_enc += time.perf_counter() - t0
+        done += 1
+    src = done * cfg["k"] * cfg["t"]
+    return {"value": src / t_enc / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": "%d of %d stripes of %s (%.1f MB source), single-threaded C oracle, %.1f s"
+                      % (done, S, cfg["name"], src / 1e6, t_enc)}
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    steps, warm = args.steps, args.warmup
+    per_step = max(0.5, args.ref_seconds / max(1, steps))
+    for _ in range(warm):
+        cpu_oracle_sample(cfg, 0.0, max_stripes=1)
+    vals = [cpu_oracle_sample(cfg, per_step) for _ in range(steps)]
+    v = statistics.median(x["value"] for x in vals)
+    cb = dict(vals[0])
+    cb["value"] = v
+    cb["sample"] = "per step: " + vals[0]["sample"]
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+           "steps": steps, "warmup": warm, "higher_is_better": True, "scaling": args.scaling,
+           "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded splitmix64 bytes, DESIGN.md R4)",
+           "config": {"workload": cfg["name"], "k": cfg["k"], "p": cfg["p"], "n": cfg["n"],
+                      "t": cfg["t"], "stripes_per_gpu": cfg["stripes"]},
+           "cpu_baseline": cb,
+           "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "smem", "global"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=60.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = configs.get(args.config)
+
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    ws, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    g = _graph(cfg, ws, rank, dev)
+    if args.variant != "auto":
+        g.set_variant(fsb.VARIANT_SMEM if args.variant == "smem" else fsb.VARIANT_GLOBAL)
+    s0, S = _shard(args, cfg, ws, rank)
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    data = inputs.stripe_data(cfg, stripe_begin=s0, num_stripes=S, device=dev)
+    chk = torch.empty((S, p, t), dtype=torch.uint8, device=dev) if p else None
+    cod = torch.empty((S, n, t), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        g.encode_stripes(data, chk, cod, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    launches_per_step = fsb.last_launch_count()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with torch.cuda.stream(stream):
+        evs[0].record(stream)
+        for i in range(args.steps):
+            step()
+            evs[i + 1].record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = evs[0].elapsed_time(evs[-1])
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    t_max = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    total_ms = float(t_max.item())
+    ms_per_step = total_ms / args.steps
+    src_bytes_all = ws * S * k * t if args.scaling == "weak" else cfg["stripes"] * k * t
+    value = src_bytes_all / (ms_per_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel: algorithmic HBM bytes per launch / mean launch time
+    inf = g.info()
+    b_hbm = S * (k + p + n) * t
+    b_gather = S * ((inf["lt_nnz"] + inf["pre_nnz"]) * t)
+    launch_ms = statistics.mean(per)
+    peak, peak_src = _peaks()
+    achieved = b_hbm / (launch_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(cfg["name"], {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "algorithmic_bytes_per_launch": b_hbm, "peak_source": peak_src,
+            "kernel": "fsb_smem_encode" if launches_per_step == 1 else "fsb_precode_global+fsb_lt_global",
+            "gather": {"bytes_per_launch": b_gather,
+                       "achieved": round(b_gather / (launch_ms * 1e-3) / 1e9, 1),
+                       "peak": SMEM_GATHER_PEAK_GBS, "unit": "GB/s",
+                       "frac": round(b_gather / (launch_ms * 1e-3) / 1e9 / SMEM_GATHER_PEAK_GBS, 4),
+                       "peak_source": "measured smem random-row gather, tools/microbench/mb.cu"}}
+
+    # e2e: host (pinned) buffers through the public API, copies inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e = _e2e(g, cfg, data, cod, S, args, dev, ws)
+
+    out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+           "scaling": args.scaling, "vs_baseline": None, "dtype": "u8",
+           "data": "synthetic (seeded splitmix64 bytes, DESIGN.md R4)",
+           "config": {"workload": cfg["name"], "k": k, "p": p, "d_p": cfg["d_p"], "n": n, "t": t,
+                      "dist": "RSD" if cfg["dist"] == configs.RSD else "Omega", "stripes_per_gpu": S,
+                      "stripes_total": S * ws if args.scaling == "weak" else cfg["stripes"],
+                      "parallelism": "stripe-sharded x%d" % ws, "variant": args.variant,
+                      "l2": "inputs (%.2f GB) exceed the 126 MB L2; no flush needed" % (S * k * t / 1e9),
+                      "lt_nnz": inf["lt_nnz"], "max_degree": inf["max_degree"]},
+           "roofline": roof, "gpu_launches": launches_per_step * args.steps,
+           "step_ms_median": round(statistics.median(per), 5), "clocks": clk, "e2e": e2e}
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_oracle_sample(cfg, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def _e2e(g, cfg, data, cod, S, args, dev, ws):
+    """Same metric through fs_encode_stripes with HOST buffers: per step, H2D of the step's
+    data from pinned memory, the encode, and D2H of checks + coded, pipelined over chunks of
+    stripes on two streams."""
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    h_data = torch.empty((S, k, t), dtype=torch.uint8, pin_memory=True)
+    h_data.copy_(data.cpu())
+    h_chk = torch.empty((S, p, t), dtype=torch.uint8, pin_memory=True) if p else None
+    h_cod = torch.empty((S, n, t), dtype=torch.uint8, pin_memory=True)
+    nchunks = min(S, 16)
+    bounds = [(i * S // nchunks, (i + 1) * S // nchunks) for i in range(nchunks)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    cs = max(b - a for a, b in bounds)
+    d_buf = [torch.empty((cs, k, t), dtype=torch.uint8, device=dev) for _ in range(2)]
+    c_buf = [torch.empty((cs, p, t), dtype=torch.uint8, device=dev) if p else None for _ in range(2)]
+    y_buf = [torch.empty((cs, n, t), dtype=torch.uint8, device=dev) for _ in range(2)]
+
+    def one_step():
+        for i, (a, b) in enumerate(bounds):
+            st = streams[i % 2]
+            with torch.cuda.stream(st):
+                db = d_buf[i % 2][:b - a]
+                db.copy_(h_data[a:b], non_blocking=True)
+                cb = c_buf[i % 2][:b - a] if p else None
+                yb = y_buf[i % 2][:b - a]
+                g.encode_stripes(db, cb, yb, stream=st)
+                if p:
+                    h_chk[a:b].copy_(cb, non_blocking=True)
+                h_cod[a:b].copy_(yb, non_blocking=True)
+
+    one_step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    cur = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cur)
+    for st in streams:
+        st.wait_stream(cur)
+    for _ in range(args.e2e_steps):
+        one_step()
+    for st in streams:
+        cur.wait_stream(st)
+    e1.record(cur)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    tm = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm.item()) / args.e2e_steps
+    # spot-check the host result against the device-resident run
+    ok = bool(torch.equal(h_cod[0].to(dev), cod[0]) and torch.equal(h_cod[S - 1].to(dev), cod[S - 1]))
+    return {"value": round(ws * S * k * t / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": S * k * t, "d2h_bytes_per_step": S * (p + n) * t,
+            "ms_per_step": round(ms, 3), "api": "fs_encode_stripes on pinned-host staging, %d chunks x 2 streams"
+            % nchunks, "checked": ok}
+
+
+if __name__ == "__main__":
+    main()

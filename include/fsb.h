@@ -1,0 +1,170 @@
+/*
+ * fsb.h -- C ABI of libfsb200.so, the B200-native Founsure 1.0 encode path
+ * (arXiv 1702.07409).  Plain C types only: host pointers, device pointers, sizes.
+ *
+ * What the library computes (§2.2, Fig. 1, steps (1) and (2)):
+ *
+ *   precode ("Check #1"):  C_i = XOR_{m in P(i)} D_m            for i < p
+ *   LT / LDGM stage:       Y_j = XOR_{m in N(j)} I_m            for j < n,
+ *                          I = [D_0 .. D_{k-1}, C_0 .. C_{p-1}]  (K = k+p symbols)
+ *
+ * bytewise over t-byte symbols, for every stripe ("partition") with the
+ * same graph.  The graph is drawn from a seeded PRNG: every check has d_p
+ * distinct data neighbours; every coded symbol has a degree drawn from the Robust Soliton
+ * distribution or a finite max-degree Omega(x), and that
+ * many distinct neighbours among the K intermediate symbols.  Conventions for everything
+ * the paper leaves open (PRNG, sampling, CDF arithmetic, stream order) are DESIGN.md §3
+ * readings R2-R15.
+ *
+ * Notation: k = data symbols (paper b), p = precode checks (paper k-b),
+ * n = coded symbols, t = bytes per symbol, S = stripes.
+ *
+ * Memory layout of every symbol block: symbol-major, t contiguous bytes per symbol
+ * (reading R13).  Data of stripe s starts at d_data + s*data_stride, etc.
+ *
+ * Ownership: the library owns fs_graph (host CSR, device CSR, device work schedules,
+ * allocated on the device current at creation).  The caller owns every data / check /
+ * coded buffer.  The library never allocates caller-visible memory and never
+ * synchronises the caller's stream; kernels are enqueued on the stream given.
+ *
+ * Errors: every call returns fs_status (0 = OK).  Validation failures return FS_EINVAL /
+ * FS_EDIST without side effects; launch failures return FS_ECUDA.  Asynchronous kernel
+ * faults surface at the caller's next synchronisation.  fs_last_error() returns a
+ * thread-local message describing the last failure on the calling thread.
+ *
+ * Thread safety: a graph is immutable after creation (except fs_graph_set_variant, which
+ * must not race with encodes); concurrent fs_encode* calls on different streams are fine.
+ * Output is deterministic and independent of stream, launch configuration, kernel
+ * variant and GPU count (XOR is exact, associative and commutative).
+ */
+#ifndef FSB_H_
+#define FSB_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FSB_API __attribute__((visibility("default")))
+#else
+#define FSB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FS_OK = 0,
+  FS_EINVAL = -1,       /* invalid argument (sizes, alignment, strides, pointers)          */
+  FS_EDIST = -2,        /* invalid degree distribution                                    */
+  FS_ENOMEM = -3,       /* host or device allocation failed                                */
+  FS_ECUDA = -4,        /* CUDA runtime / launch error (message in fs_last_error())        */
+  FS_EUNSUPPORTED = -5  /* operation not available for this graph (e.g. host-only graph)   */
+} fs_status;
+
+typedef enum { FS_DIST_RSD = 1, FS_DIST_FINITE = 2 } fs_dist_kind;
+
+/* Code parameters: the paper's problem statement. */
+typedef struct {
+  uint32_t k;             /* data symbols (paper b); >= 1                                     */
+  uint32_t p;             /* precode checks (paper k-b); 0 = no precode                       */
+  uint32_t d_p;           /* data neighbours per check; 1 <= d_p <= k when p > 0             */
+  uint32_t n;             /* coded symbols; >= 1                                              */
+  uint64_t t;             /* bytes per symbol; multiple of 16                                 */
+  int32_t dist;           /* fs_dist_kind                                                     */
+  double rsd_c;           /* RSD: c > 0                                                       */
+  double rsd_delta;       /* RSD: 0 < delta < 1                                               */
+  const uint32_t *fin_deg;   /* FINITE: support degrees, strictly increasing, >= 1           */
+  const double *fin_prob;    /* FINITE: weights >= 0, sum within 1e-5 of 1 (normalised)      */
+  uint32_t fin_len;          /* FINITE: number of support points                             */
+  uint64_t seed;          /* splitmix64 graph seed (reading R2/R3)                            */
+} fs_params;
+
+typedef struct fs_graph fs_graph;  /* opaque */
+
+/* Graph-creation flags. */
+#define FS_GRAPH_HOST_ONLY 1u   /* build host CSR only: no device memory, no CUDA calls.
+                                   fs_encode* then return FS_EUNSUPPORTED.               */
+
+/* Kernel variants (fs_graph_set_variant).  All produce identical bytes. */
+#define FS_VARIANT_AUTO 0       /* per call: SMEM when eligible and the call has >= 2 tiles
+                                   per SM, else GLOBAL                                   */
+#define FS_VARIANT_SMEM 1       /* persistent TMA-staged shared-memory tile kernel        */
+#define FS_VARIANT_GLOBAL 2     /* L2-resident band sweep (precode kernel + LT kernel)    */
+
+/* Seeded graph generation (step a1): precode rows first, then LT rows (reading R5), each
+ * neighbour list sorted ascending (R14).  Without FS_GRAPH_HOST_ONLY the CSR and the work
+ * schedules are uploaded to the current device (synchronously, before return).
+ * FS_EINVAL: k == 0, n == 0, t == 0 or t % 16 != 0, p > 0 with d_p == 0 or d_p > k,
+ *            K = k+p >= 2^31.
+ * FS_EDIST:  empty support, degree 0, degrees not strictly increasing, negative weight,
+ *            |sum - 1| > 1e-5, RSD c <= 0, delta outside (0,1), R/delta <= 1, K/R < 1.   */
+FSB_API fs_status fs_graph_create(const fs_params *prm, uint32_t flags, fs_graph **out);
+
+/* Build a graph from CSR arrays (e.g. received by NCCL broadcast from rank 0).
+ * pre_row_ptr[p+1], pre_col[p*d_p] (indices in [0,k)), lt_row_ptr[n+1], lt_col[nnz]
+ * (indices in [0,K)); rows need not be sorted but must hold distinct indices.
+ * The arrays are copied.  FS_EINVAL on any structural violation.                         */
+FSB_API fs_status fs_graph_from_csr(const fs_params *prm, const int32_t *pre_row_ptr,
+                            const int32_t *pre_col, const int32_t *lt_row_ptr,
+                            const int32_t *lt_col, uint32_t flags, fs_graph **out);
+
+/* Host views of the graph's CSR (owned by g, valid until fs_free(g)).  Any out pointer may
+ * be NULL.  pre_* are NULL-or-empty when p == 0.                                            */
+FSB_API fs_status fs_graph_csr(const fs_graph *g, const int32_t **pre_row_ptr, const int32_t **pre_col,
+                       const int32_t **lt_row_ptr, const int32_t **lt_col, uint64_t *lt_nnz);
+
+/* Summary numbers of a graph (for rooflines and reports). */
+typedef struct {
+  uint32_t k, p, d_p, n;
+  uint64_t t;
+  uint64_t lt_nnz;           /* edges of the LT graph                                         */
+  uint64_t pre_nnz;          /* edges of the precode graph (p*d_p)                            */
+  uint32_t max_degree;       /* largest LT row degree                                         */
+  int32_t variant;           /* FS_VARIANT_* currently set                                    */
+  int32_t smem_eligible;     /* 1 when the SMEM variant can run this graph                    */
+  uint32_t smem_bytes;       /* dynamic shared memory of the SMEM kernel                      */
+  uint32_t sched_bytes;      /* size of the SMEM kernel's work schedule                       */
+  uint32_t sched_steps_max;  /* SMEM schedule: steps of the most loaded warp per tile         */
+  uint32_t sched_steps_avg;  /* SMEM schedule: mean steps per warp per tile (x1, rounded)     */
+  int32_t device;            /* CUDA device of the device copy, -1 for host-only graphs       */
+} fs_graph_info;
+
+FSB_API fs_status fs_graph_get_info(const fs_graph *g, fs_graph_info *info);
+
+/* Force a kernel variant (FS_VARIANT_*).  FS_EUNSUPPORTED if SMEM is requested for a graph
+ * that is not eligible (t % 128 != 0, n > 65535 or the tile does not fit shared memory). */
+FSB_API fs_status fs_graph_set_variant(fs_graph *g, int32_t variant);
+
+/* One stripe, coded rows [row_begin, row_end) (row partition across GPUs).
+ * d_data:   k*t bytes on the graph's device, 16-B aligned.
+ * d_checks: p*t bytes (all p checks are always computed and written); NULL iff p == 0.
+ * d_coded:  (row_end-row_begin)*t bytes; row j is written at d_coded + (j-row_begin)*t.
+ * stream:   a cudaStream_t (NULL = legacy default stream).
+ * Launches: GLOBAL = 1 precode kernel (if p > 0) + 1 LT kernel; SMEM = 1 fused kernel.   */
+FSB_API fs_status fs_encode(const fs_graph *g, const uint8_t *d_data, uint8_t *d_checks,
+                    uint8_t *d_coded, uint32_t row_begin, uint32_t row_end, void *stream);
+
+/* num_stripes stripes with the same graph.  Strides are in bytes and must be
+ * multiples of 16 and >= k*t, p*t, n*t respectively.  0 stripes is a no-op.               */
+FSB_API fs_status fs_encode_stripes(const fs_graph *g, uint32_t num_stripes,
+                            const uint8_t *d_data, uint64_t data_stride,
+                            uint8_t *d_checks, uint64_t checks_stride,
+                            uint8_t *d_coded, uint64_t coded_stride, void *stream);
+
+/* Number of kernel launches the last successful fs_encode / fs_encode_stripes on this
+ * thread enqueued (for launch accounting in benchmarks).                                 */
+FSB_API uint32_t fs_last_launch_count(void);
+
+/* Frees everything g owns (device memory on its device).  NULL-safe.                     */
+FSB_API void fs_free(fs_graph *g);
+
+/* Thread-local description of the last error ("" if none). */
+FSB_API const char *fs_last_error(void);
+
+/* Library version string. */
+FSB_API const char *fs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSB_H_ */

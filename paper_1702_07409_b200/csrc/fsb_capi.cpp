@@ -1,0 +1,232 @@
+// C ABI of libfsb200.so (include/fsb.h): argument validation, ownership, error reporting.
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "fsb_internal.h"
+
+namespace fsb {
+namespace {
+thread_local std::string g_err;
+thread_local uint32_t g_launches = 0;
+}  // namespace
+void set_error(const std::string &msg) { g_err = msg; }
+}  // namespace fsb
+
+using fsb::set_error;
+
+namespace {
+
+fs_status finish_create(fs_graph *h, uint32_t flags, fs_graph **out) {
+  fsb::Graph &g = h->g;
+  fsb::build_smem_schedule(g);
+  if (!(flags & FS_GRAPH_HOST_ONLY)) {
+    fs_status st = fsb::upload_graph(g);
+    if (st != FS_OK) {
+      fsb::free_device(g);
+      delete h;
+      return st;
+    }
+  } else {
+    g.dev.device = -1;
+  }
+  *out = h;
+  return FS_OK;
+}
+
+fs_graph *new_graph(const fs_params *prm) {
+  fs_graph *h = new (std::nothrow) fs_graph();
+  if (!h) return nullptr;
+  fsb::Graph &g = h->g;
+  g.prm = *prm;
+  if (prm->dist == FS_DIST_FINITE && prm->fin_len && prm->fin_deg && prm->fin_prob) {
+    g.fin_deg.assign(prm->fin_deg, prm->fin_deg + prm->fin_len);
+    g.fin_prob.assign(prm->fin_prob, prm->fin_prob + prm->fin_len);
+    g.prm.fin_deg = g.fin_deg.data();
+    g.prm.fin_prob = g.fin_prob.data();
+  } else {
+    g.prm.fin_deg = nullptr;
+    g.prm.fin_prob = nullptr;
+    g.prm.fin_len = 0;
+  }
+  return h;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+fs_status fs_graph_create(const fs_params *prm, uint32_t flags, fs_graph **out) {
+  fsb::set_error("");
+  if (!prm || !out) { set_error("null argument"); return FS_EINVAL; }
+  *out = nullptr;
+  fs_status st = fsb::validate_params(*prm);
+  if (st != FS_OK) return st;
+  fs_graph *h = new_graph(prm);
+  if (!h) { set_error("out of host memory"); return FS_ENOMEM; }
+  try {
+    st = fsb::generate_csr(h->g);
+  } catch (const std::bad_alloc &) {
+    st = FS_ENOMEM;
+    set_error("out of host memory");
+  }
+  if (st != FS_OK) {
+    delete h;
+    return st;
+  }
+  return finish_create(h, flags, out);
+}
+
+fs_status fs_graph_from_csr(const fs_params *prm, const int32_t *pre_row_ptr, const int32_t *pre_col,
+                            const int32_t *lt_row_ptr, const int32_t *lt_col, uint32_t flags, fs_graph **out) {
+  fsb::set_error("");
+  if (!prm || !out || !lt_row_ptr || !lt_col) { set_error("null argument"); return FS_EINVAL; }
+  *out = nullptr;
+  fs_status st = fsb::validate_params(*prm);
+  if (st != FS_OK) return st;
+  if (prm->p > 0 && (!pre_row_ptr || !pre_col)) { set_error("precode CSR missing"); return FS_EINVAL; }
+  fs_graph *h = new_graph(prm);
+  if (!h) { set_error("out of host memory"); return FS_ENOMEM; }
+  fsb::Graph &g = h->g;
+  const uint32_t p = prm->p, n = prm->n;
+  if (p) {
+    g.pre_row_ptr.assign(pre_row_ptr, pre_row_ptr + p + 1);
+    if (g.pre_row_ptr[p] < 0) { delete h; set_error("invalid precode CSR"); return FS_EINVAL; }
+    g.pre_col.assign(pre_col, pre_col + g.pre_row_ptr[p]);
+  } else {
+    g.pre_row_ptr.assign(1, 0);
+  }
+  g.lt_row_ptr.assign(lt_row_ptr, lt_row_ptr + n + 1);
+  if (g.lt_row_ptr[n] < 0) { delete h; set_error("invalid LT CSR"); return FS_EINVAL; }
+  g.lt_col.assign(lt_col, lt_col + g.lt_row_ptr[n]);
+  st = fsb::validate_csr(g);
+  if (st != FS_OK) {
+    delete h;
+    return st;
+  }
+  g.max_degree = 0;
+  for (uint32_t j = 0; j < n; ++j)
+    g.max_degree = std::max<uint32_t>(g.max_degree, static_cast<uint32_t>(g.lt_row_ptr[j + 1] - g.lt_row_ptr[j]));
+  return finish_create(h, flags, out);
+}
+
+fs_status fs_graph_csr(const fs_graph *h, const int32_t **pre_row_ptr, const int32_t **pre_col,
+                       const int32_t **lt_row_ptr, const int32_t **lt_col, uint64_t *lt_nnz) {
+  if (!h) { set_error("null graph"); return FS_EINVAL; }
+  const fsb::Graph &g = h->g;
+  if (pre_row_ptr) *pre_row_ptr = g.pre_row_ptr.data();
+  if (pre_col) *pre_col = g.pre_col.empty() ? nullptr : g.pre_col.data();
+  if (lt_row_ptr) *lt_row_ptr = g.lt_row_ptr.data();
+  if (lt_col) *lt_col = g.lt_col.data();
+  if (lt_nnz) *lt_nnz = g.lt_col.size();
+  return FS_OK;
+}
+
+fs_status fs_graph_get_info(const fs_graph *h, fs_graph_info *info) {
+  if (!h || !info) { set_error("null argument"); return FS_EINVAL; }
+  const fsb::Graph &g = h->g;
+  std::memset(info, 0, sizeof(*info));
+  info->k = g.prm.k;
+  info->p = g.prm.p;
+  info->d_p = g.prm.d_p;
+  info->n = g.prm.n;
+  info->t = g.prm.t;
+  info->lt_nnz = g.lt_col.size();
+  info->pre_nnz = g.pre_col.size();
+  info->max_degree = g.max_degree;
+  info->variant = g.variant;
+  info->smem_eligible = g.smem_eligible ? 1 : 0;
+  info->smem_bytes = g.smem_bytes;
+  info->sched_bytes = static_cast<uint32_t>(g.sched.words.size() * 2);
+  info->sched_steps_max = g.sched.steps_max;
+  info->sched_steps_avg = (g.sched.steps_total + fsb::kConsumerWarps / 2) / fsb::kConsumerWarps;
+  info->device = g.dev.device;
+  return FS_OK;
+}
+
+fs_status fs_graph_set_variant(fs_graph *h, int32_t variant) {
+  if (!h) { set_error("null graph"); return FS_EINVAL; }
+  if (variant != FS_VARIANT_AUTO && variant != FS_VARIANT_SMEM && variant != FS_VARIANT_GLOBAL) {
+    set_error("unknown variant");
+    return FS_EINVAL;
+  }
+  if (variant == FS_VARIANT_SMEM && !h->g.smem_eligible) {
+    set_error("SMEM variant not eligible for this graph");
+    return FS_EUNSUPPORTED;
+  }
+  h->g.variant = variant;
+  return FS_OK;
+}
+
+static fs_status check_device_graph(const fs_graph *h) {
+  if (!h) { set_error("null graph"); return FS_EINVAL; }
+  if (h->g.dev.device < 0) { set_error("host-only graph has no device copy"); return FS_EUNSUPPORTED; }
+  return FS_OK;
+}
+
+fs_status fs_encode(const fs_graph *h, const uint8_t *d_data, uint8_t *d_checks, uint8_t *d_coded,
+                    uint32_t row_begin, uint32_t row_end, void *stream) {
+  fsb::set_error("");
+  fsb::g_launches = 0;
+  fs_status st = check_device_graph(h);
+  if (st != FS_OK) return st;
+  const fsb::Graph &g = h->g;
+  if (row_begin > row_end || row_end > g.prm.n) { set_error("invalid row range"); return FS_EINVAL; }
+  if (!d_data || !aligned16(d_data)) { set_error("d_data must be a 16-B aligned device pointer"); return FS_EINVAL; }
+  if (g.prm.p > 0 && (!d_checks || !aligned16(d_checks))) { set_error("d_checks must be 16-B aligned, non-NULL when p > 0"); return FS_EINVAL; }
+  if (g.prm.p == 0 && d_checks) { set_error("d_checks must be NULL when p == 0"); return FS_EINVAL; }
+  if (row_end > row_begin && (!d_coded || !aligned16(d_coded))) { set_error("d_coded must be a 16-B aligned device pointer"); return FS_EINVAL; }
+  const uint64_t t = g.prm.t;
+  uint32_t launches = 0;
+  st = fsb::launch_encode(g, 1, d_data, g.prm.k * t, d_checks, g.prm.p * t, d_coded,
+                          static_cast<uint64_t>(row_end - row_begin) * t, row_begin, row_end, stream, &launches);
+  if (st == FS_OK) fsb::g_launches = launches;
+  return st;
+}
+
+fs_status fs_encode_stripes(const fs_graph *h, uint32_t S, const uint8_t *d_data, uint64_t data_stride,
+                            uint8_t *d_checks, uint64_t checks_stride, uint8_t *d_coded, uint64_t coded_stride,
+                            void *stream) {
+  fsb::set_error("");
+  fsb::g_launches = 0;
+  fs_status st = check_device_graph(h);
+  if (st != FS_OK) return st;
+  const fsb::Graph &g = h->g;
+  if (S == 0) return FS_OK;
+  const uint64_t t = g.prm.t;
+  if (!d_data || !aligned16(d_data) || data_stride < g.prm.k * t || data_stride % 16) {
+    set_error("d_data must be 16-B aligned with data_stride >= k*t, a multiple of 16");
+    return FS_EINVAL;
+  }
+  if (g.prm.p > 0 && (!d_checks || !aligned16(d_checks) || checks_stride < g.prm.p * t || checks_stride % 16)) {
+    set_error("d_checks must be 16-B aligned with checks_stride >= p*t, a multiple of 16");
+    return FS_EINVAL;
+  }
+  if (g.prm.p == 0 && d_checks) { set_error("d_checks must be NULL when p == 0"); return FS_EINVAL; }
+  if (!d_coded || !aligned16(d_coded) || coded_stride < g.prm.n * t || coded_stride % 16) {
+    set_error("d_coded must be 16-B aligned with coded_stride >= n*t, a multiple of 16");
+    return FS_EINVAL;
+  }
+  uint32_t launches = 0;
+  st = fsb::launch_encode(g, S, d_data, data_stride, d_checks, checks_stride, d_coded, coded_stride, 0, g.prm.n,
+                          stream, &launches);
+  if (st == FS_OK) fsb::g_launches = launches;
+  return st;
+}
+
+uint32_t fs_last_launch_count(void) { return fsb::g_launches; }
+
+void fs_free(fs_graph *h) {
+  if (!h) return;
+  fsb::free_device(h->g);
+  delete h;
+}
+
+const char *fs_last_error(void) { return fsb::g_err.c_str(); }
+
+const char *fs_version(void) { return "fsb200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

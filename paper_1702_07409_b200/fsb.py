@@ -1,0 +1,216 @@
+"""Thin Python binding of libfsb200.so (include/fsb.h) -- argument marshalling only.
+
+Every step of the encode runs in the library's CUDA kernels; PyTorch supplies device
+memory (uint8 CUDA tensors) and streams.  There is no CPU fallback: if the extension is
+missing or a call fails, this module raises.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfsb200.so")
+
+FS_OK, FS_EINVAL, FS_EDIST, FS_ENOMEM, FS_ECUDA, FS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
+FS_DIST_RSD, FS_DIST_FINITE = 1, 2
+FS_GRAPH_HOST_ONLY = 1
+VARIANT_AUTO, VARIANT_SMEM, VARIANT_GLOBAL = 0, 1, 2
+
+# Every symbol include/fsb.h declares (checked by tests/test_capi.py).
+EXPORTS = ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get_info",
+           "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_last_launch_count",
+           "fs_free", "fs_last_error", "fs_version")
+
+
+class FsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("fsb error %d: %s" % (status, msg))
+        self.status = status
+
+
+class fs_params(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_uint32), ("p", ctypes.c_uint32), ("d_p", ctypes.c_uint32),
+                ("n", ctypes.c_uint32), ("t", ctypes.c_uint64), ("dist", ctypes.c_int32),
+                ("rsd_c", ctypes.c_double), ("rsd_delta", ctypes.c_double),
+                ("fin_deg", ctypes.POINTER(ctypes.c_uint32)),
+                ("fin_prob", ctypes.POINTER(ctypes.c_double)), ("fin_len", ctypes.c_uint32),
+                ("seed", ctypes.c_uint64)]
+
+
+class fs_graph_info(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_uint32), ("p", ctypes.c_uint32), ("d_p", ctypes.c_uint32),
+                ("n", ctypes.c_uint32), ("t", ctypes.c_uint64), ("lt_nnz", ctypes.c_uint64),
+                ("pre_nnz", ctypes.c_uint64), ("max_degree", ctypes.c_uint32),
+                ("variant", ctypes.c_int32), ("smem_eligible", ctypes.c_int32),
+                ("smem_bytes", ctypes.c_uint32), ("sched_bytes", ctypes.c_uint32),
+                ("sched_steps_max", ctypes.c_uint32), ("sched_steps_avg", ctypes.c_uint32),
+                ("device", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libfsb200.so (fails loudly if it was not built: run __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libfsb200.so not built at %s (run __graft_entry__.build())" % LIB_PATH)
+        L = ctypes.CDLL(LIB_PATH)
+        P, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
+        PP = ctypes.POINTER(ctypes.c_void_p)
+        L.fs_graph_create.argtypes = [ctypes.POINTER(fs_params), u32, PP]
+        L.fs_graph_from_csr.argtypes = [ctypes.POINTER(fs_params), P, P, P, P, u32, PP]
+        L.fs_graph_csr.argtypes = [P, PP, PP, PP, PP, ctypes.POINTER(u64)]
+        L.fs_graph_get_info.argtypes = [P, ctypes.POINTER(fs_graph_info)]
+        L.fs_graph_set_variant.argtypes = [P, i32]
+        L.fs_encode.argtypes = [P, P, P, P, u32, u32, P]
+        L.fs_encode_stripes.argtypes = [P, u32, P, u64, P, u64, P, u64, P]
+        for f in ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get_info",
+                  "fs_graph_set_variant", "fs_encode", "fs_encode_stripes"):
+            getattr(L, f).restype = ctypes.c_int
+        L.fs_last_launch_count.restype = u32
+        L.fs_last_launch_count.argtypes = []
+        L.fs_free.argtypes = [P]
+        L.fs_free.restype = None
+        L.fs_last_error.restype = ctypes.c_char_p
+        L.fs_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(st):
+    if st != FS_OK:
+        raise FsError(st, lib().fs_last_error().decode())
+
+
+def last_launch_count():
+    return int(lib().fs_last_launch_count())
+
+
+def _ptr(x):
+    """Device pointer of a CUDA tensor (None -> NULL)."""
+    if x is None:
+        return None
+    if not x.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not x.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_params(cfg):
+    """fs_params from a config dict (keys of configs.get())."""
+    prm = fs_params()
+    prm.k, prm.p, prm.d_p, prm.n, prm.t = cfg["k"], cfg["p"], cfg.get("d_p", 0), cfg["n"], cfg["t"]
+    prm.dist = cfg["dist"]
+    prm.rsd_c = cfg.get("rsd_c", 0.0)
+    prm.rsd_delta = cfg.get("rsd_delta", 0.0)
+    fd = np.ascontiguousarray(cfg.get("fin_deg", ()), dtype=np.uint32)
+    fp = np.ascontiguousarray(cfg.get("fin_prob", ()), dtype=np.float64)
+    prm._keep = (fd, fp)
+    if len(fd):
+        prm.fin_deg = fd.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+        prm.fin_prob = fp.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    prm.fin_len = len(fd)
+    prm.seed = cfg["seed"]
+    return prm
+
+
+class Graph:
+    """Owner of an fs_graph handle."""
+
+    def __init__(self, handle, cfg):
+        self._h = handle
+        self.cfg = dict(cfg)
+        self.k, self.p, self.n, self.t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+        self.d_p = cfg.get("d_p", 0)
+        self.K = self.k + self.p
+
+    @classmethod
+    def create(cls, cfg, host_only=False):
+        """fs_graph_create: seeded generation (+ upload to the current CUDA device)."""
+        prm = make_params(cfg)
+        h = ctypes.c_void_p()
+        _check(lib().fs_graph_create(ctypes.byref(prm), FS_GRAPH_HOST_ONLY if host_only else 0,
+                                     ctypes.byref(h)))
+        return cls(h, cfg)
+
+    @classmethod
+    def from_csr(cls, cfg, pre_row_ptr, pre_col, lt_row_ptr, lt_col, host_only=False):
+        """fs_graph_from_csr (e.g. after an NCCL broadcast of the CSR)."""
+        prm = make_params(cfg)
+        arrs = [np.ascontiguousarray(a, dtype=np.int32) for a in (pre_row_ptr, pre_col, lt_row_ptr, lt_col)]
+        ptrs = [a.ctypes.data_as(ctypes.c_void_p) if a.size else None for a in arrs]
+        h = ctypes.c_void_p()
+        _check(lib().fs_graph_from_csr(ctypes.byref(prm), *ptrs, FS_GRAPH_HOST_ONLY if host_only else 0,
+                                       ctypes.byref(h)))
+        return cls(h, cfg)
+
+    def csr(self):
+        """(pre_row_ptr, pre_col, lt_row_ptr, lt_col) as numpy int32 copies."""
+        ptrs = [ctypes.c_void_p() for _ in range(4)]
+        nnz = ctypes.c_uint64()
+        _check(lib().fs_graph_csr(self._h, *[ctypes.byref(x) for x in ptrs], ctypes.byref(nnz)))
+
+        def arr(p, n):
+            if n == 0 or not p.value:
+                return np.zeros(0, np.int32)
+            return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_int32)), (n,)).copy()
+
+        pre_rp = arr(ptrs[0], self.p + 1)
+        pre_c = arr(ptrs[1], self.p * self.d_p if self.p else 0)
+        lt_rp = arr(ptrs[2], self.n + 1)
+        lt_c = arr(ptrs[3], int(nnz.value))
+        return pre_rp, pre_c, lt_rp, lt_c
+
+    def info(self):
+        inf = fs_graph_info()
+        _check(lib().fs_graph_get_info(self._h, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in fs_graph_info._fields_}
+
+    def set_variant(self, variant):
+        _check(lib().fs_graph_set_variant(self._h, variant))
+
+    def encode(self, data, checks, coded, row_begin=0, row_end=None, stream=None):
+        """fs_encode: one stripe, coded rows [row_begin, row_end) into `coded`."""
+        row_end = self.n if row_end is None else row_end
+        _check(lib().fs_encode(self._h, _ptr(data), _ptr(checks), _ptr(coded), row_begin, row_end,
+                               _stream(stream)))
+
+    def encode_stripes(self, data, checks, coded, stream=None):
+        """fs_encode_stripes over contiguous [S,k,t] / [S,p,t] / [S,n,t] uint8 CUDA tensors."""
+        S = data.shape[0]
+        t = self.t
+        _check(lib().fs_encode_stripes(self._h, S, _ptr(data), self.k * t, _ptr(checks), self.p * t,
+                                       _ptr(coded), self.n * t, _stream(stream)))
+
+    def encode_stripes_raw(self, S, data_ptr, data_stride, checks_ptr, checks_stride, coded_ptr,
+                           coded_stride, stream=None):
+        """fs_encode_stripes with explicit device pointers and byte strides."""
+        _check(lib().fs_encode_stripes(self._h, S, ctypes.c_void_p(data_ptr), data_stride,
+                                       ctypes.c_void_p(checks_ptr) if checks_ptr else None,
+                                       checks_stride, ctypes.c_void_p(coded_ptr), coded_stride,
+                                       _stream(stream)))
+
+    def free(self):
+        if self._h:
+            lib().fs_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def version():
+    return lib().fs_version().decode()

@@ -1,0 +1,149 @@
+"""Host-side tests of the C ABI (no GPU): the library loads, exports every symbol of
+include/fsb.h, validates its arguments, and its host graph generator reproduces the
+oracle's CSR byte for byte -- two independent implementations."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1702_07409_b200 import configs, fsb
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "fsb.h")).read()
+    return sorted(set(re.findall(r"FSB_API\s+[\w\s\*]+?\b(fs_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+    L = fsb.lib()
+    declared = _declared_symbols()
+    assert len(declared) >= 10
+    assert sorted(fsb.EXPORTS) == declared
+    for name in declared:
+        assert hasattr(L, name), name
+        assert ctypes.cast(getattr(L, name), ctypes.c_void_p).value
+    assert "sm_100a" in fsb.version()
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_library_generator_matches_oracle(cid):
+    """P2: CSR equality, library (C++) vs oracle (C), all five configs."""
+    c = configs.get(cid)
+    g = fsb.Graph.create(c, host_only=True)
+    o = oracle.generate_graph(c)
+    pre_rp, pre_c, lt_rp, lt_c = g.csr()
+    assert np.array_equal(lt_rp, o.lt_row_ptr) and np.array_equal(lt_c, o.lt_col)
+    if c["p"]:
+        assert np.array_equal(pre_rp, o.pre_row_ptr) and np.array_equal(pre_c, o.pre_col)
+    inf = g.info()
+    assert inf["lt_nnz"] == o.nnz and inf["max_degree"] == int(np.diff(o.lt_row_ptr).max())
+    assert inf["device"] == -1
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_library_generator_matches_oracle_random_params(seed):
+    rng = np.random.default_rng(seed)
+    k = int(rng.integers(1, 300))
+    p = int(rng.integers(0, 20))
+    dp = int(rng.integers(1, min(k, 5) + 1))
+    n = int(rng.integers(1, 400))
+    if seed % 2:
+        c = dict(k=k, p=p, d_p=dp, n=n, t=64, dist=configs.FINITE, seed=int(rng.integers(0, 2**63)),
+                 fin_deg=configs.OMEGA_DEGREES, fin_prob=configs.OMEGA_PROBS)
+    else:
+        c = dict(k=max(k, 8), p=p, d_p=dp, n=n, t=64, dist=configs.RSD, seed=int(rng.integers(0, 2**63)),
+                 rsd_c=0.1, rsd_delta=0.1)
+    try:
+        o = oracle.generate_graph(c)
+    except ValueError:
+        with pytest.raises(fsb.FsError):
+            fsb.Graph.create(c, host_only=True)
+        return
+    g = fsb.Graph.create(c, host_only=True)
+    a = g.csr()
+    for x, y in zip(a, (o.pre_row_ptr, o.pre_col, o.lt_row_ptr, o.lt_col)):
+        if c["p"] or len(y) > 1:
+            assert np.array_equal(x, y)
+
+
+def test_from_csr_roundtrip_and_validation():
+    c = configs.get(2)
+    g = fsb.Graph.create(c, host_only=True)
+    pre_rp, pre_c, lt_rp, lt_c = g.csr()
+    g2 = fsb.Graph.from_csr(c, pre_rp, pre_c, lt_rp, lt_c, host_only=True)
+    for x, y in zip(g2.csr(), (pre_rp, pre_c, lt_rp, lt_c)):
+        assert np.array_equal(x, y)
+    bad = lt_c.copy()
+    bad[1] = bad[0]                      # duplicate in row 0
+    with pytest.raises(fsb.FsError) as e:
+        fsb.Graph.from_csr(c, pre_rp, pre_c, lt_rp, bad, host_only=True)
+    assert e.value.status == fsb.FS_EINVAL
+    bad = lt_c.copy()
+    bad[0] = c["k"] + c["p"]             # out of range
+    with pytest.raises(fsb.FsError):
+        fsb.Graph.from_csr(c, pre_rp, pre_c, lt_rp, bad, host_only=True)
+    bad = pre_c.copy()
+    bad[0] = c["k"]                      # precode index must be a data index
+    with pytest.raises(fsb.FsError):
+        fsb.Graph.from_csr(c, pre_rp, bad, lt_rp, lt_c, host_only=True)
+
+
+@pytest.mark.parametrize("override,status", [
+    (dict(k=0), fsb.FS_EINVAL),
+    (dict(n=0), fsb.FS_EINVAL),
+    (dict(t=100), fsb.FS_EINVAL),
+    (dict(t=0), fsb.FS_EINVAL),
+    (dict(p=5, d_p=0), fsb.FS_EINVAL),
+    (dict(p=5, d_p=2000), fsb.FS_EINVAL),
+    (dict(rsd_c=0.0), fsb.FS_EDIST),
+    (dict(rsd_delta=1.5), fsb.FS_EDIST),
+    (dict(dist=7), fsb.FS_EDIST),
+])
+def test_param_validation(override, status):
+    c = configs.get(2, **override)
+    with pytest.raises(fsb.FsError) as e:
+        fsb.Graph.create(c, host_only=True)
+    assert e.value.status == status
+
+
+@pytest.mark.parametrize("deg,prob", [
+    ((1, 2, 2), (0.3, 0.3, 0.4)),        # not strictly increasing
+    ((0, 2), (0.5, 0.5)),                # degree 0
+    ((1, 2), (0.5, 0.6)),                # does not sum to 1
+    ((1, 2), (-0.1, 1.1)),               # negative weight
+    ((), ()),                            # empty support
+])
+def test_finite_distribution_validation(deg, prob):
+    c = configs.get(3, fin_deg=deg, fin_prob=prob)
+    with pytest.raises(fsb.FsError) as e:
+        fsb.Graph.create(c, host_only=True)
+    assert e.value.status == fsb.FS_EDIST
+
+
+def test_baseline_omega_sum_passes():
+    """The BASELINE Omega sums to 0.999998: inside the 1e-5 tolerance (reading R9)."""
+    assert abs(sum(configs.OMEGA_PROBS) - 1) < 1e-5
+    fsb.Graph.create(configs.get(3), host_only=True)
+
+
+def test_host_only_graph_refuses_encode():
+    import ctypes
+    g = fsb.Graph.create(configs.get(1), host_only=True)
+    st = fsb.lib().fs_encode(g._h, ctypes.c_void_p(16), None, ctypes.c_void_p(16), 0, 1, None)
+    assert st == fsb.FS_EUNSUPPORTED
+    assert b"host-only" in fsb.lib().fs_last_error()
+
+
+def test_schedule_balance():
+    """The SMEM schedule covers every edge and balances warps (max within 5% of mean)."""
+    for cid in (2, 4):
+        g = fsb.Graph.create(configs.get(cid), host_only=True)
+        inf = g.info()
+        assert inf["smem_eligible"] == 1
+        assert inf["sched_steps_avg"] * 16 >= inf["lt_nnz"] // 4
+        assert inf["sched_steps_max"] <= 1.05 * inf["sched_steps_avg"] + 4

@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by element.
+
+Bar: bit-exact on every output byte (checks and coded symbols) -- the work is
+integer XOR.  Full-size configs are compared in full (the C oracle finishes them in
+seconds), in the launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1702_07409_b200 import configs, fsb, inputs
+
+pytestmark = pytest.mark.gpu
+
+_ORACLE = {}
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _oracle_case(cfg, S=None):
+    key = (tuple(sorted((k, v) for k, v in cfg.items() if not isinstance(v, tuple))), S)
+    if key not in _ORACLE:
+        g = oracle.generate_graph(cfg)
+        D = inputs.stripe_data(cfg, num_stripes=S).numpy()
+        C, Y = oracle.encode(g, D)
+        _ORACLE.clear()
+        _ORACLE[key] = (D, C, Y)
+    return _ORACLE[key]
+
+
+def _run(cfg, variant, S=None, data=None):
+    g = fsb.Graph.create(cfg)
+    if variant is not None:
+        g.set_variant(variant)
+    S = cfg["stripes"] if S is None else S
+    d = data if data is not None else inputs.stripe_data(cfg, num_stripes=S, device="cuda")
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    chk = torch.empty((S, p, t), dtype=torch.uint8, device="cuda") if p else None
+    cod = torch.empty((S, n, t), dtype=torch.uint8, device="cuda")
+    if chk is not None:
+        chk.fill_(0xA5)
+    cod.fill_(0x5A)
+    g.encode_stripes(d, chk, cod)
+    torch.cuda.synchronize()
+    return g, (chk.cpu().numpy() if chk is not None else None), cod.cpu().numpy()
+
+
+def _assert_equal(a, b, what):
+    if not np.array_equal(a, b):
+        bad = np.argwhere(a != b)
+        raise AssertionError("%s: %d mismatching bytes, first at %s" % (what, len(bad), bad[:4].tolist()))
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [fsb.VARIANT_AUTO, fsb.VARIANT_GLOBAL, fsb.VARIANT_SMEM])
+def test_config_parity(cid, variant):
+    _need_gpu()
+    cfg = configs.get(cid)
+    g = fsb.Graph.create(cfg)
+    if variant == fsb.VARIANT_SMEM and not g.info()["smem_eligible"]:
+        pytest.skip("SMEM variant not eligible for config %d" % cid)
+    D, C, Y = _oracle_case(cfg)
+    _, c, y = _run(cfg, variant)
+    if cfg["p"]:
+        _assert_equal(c, C, "checks")
+    _assert_equal(y, Y, "coded")
+
+
+def test_row_range_partition_concatenates():
+    """P10 / SURVEY §8(e): rows [r*n/G, (r+1)*n/G) per rank concatenate to the full output."""
+    _need_gpu()
+    cfg = configs.get(3)
+    g = fsb.Graph.create(cfg)
+    D, C, Y = _oracle_case(cfg)
+    d = torch.from_numpy(D[0]).cuda()
+    n, t = cfg["n"], cfg["t"]
+    for G in (2, 3, 8):
+        parts = []
+        for r in range(G):
+            a, b = r * n // G, (r + 1) * n // G
+            chk = torch.empty((cfg["p"], t), dtype=torch.uint8, device="cuda")
+            out = torch.empty((b - a, t), dtype=torch.uint8, device="cuda")
+            g.encode(d, chk, out, a, b)
+            parts.append(out)
+            _assert_equal(chk.cpu().numpy(), C[0], "checks rank %d" % r)
+        torch.cuda.synchronize()
+        _assert_equal(torch.cat(parts).cpu().numpy(), Y[0], "row partition G=%d" % G)
+
+
+def test_stripes_equal_single_encodes():
+    """P10: fs_encode_stripes over S stripes = S independent fs_encode calls."""
+    _need_gpu()
+    cfg = configs.get(4)
+    g = fsb.Graph.create(cfg)
+    S = 5
+    d = inputs.stripe_data(cfg, num_stripes=S, device="cuda")
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    for variant in (fsb.VARIANT_SMEM, fsb.VARIANT_GLOBAL):
+        g.set_variant(variant)
+        chk = torch.empty((S, p, t), dtype=torch.uint8, device="cuda")
+        cod = torch.empty((S, n, t), dtype=torch.uint8, device="cuda")
+        g.encode_stripes(d, chk, cod)
+        for s in range(S):
+            c1 = torch.empty((p, t), dtype=torch.uint8, device="cuda")
+            y1 = torch.empty((n, t), dtype=torch.uint8, device="cuda")
+            g.encode(d[s], c1, y1)
+            torch.cuda.synchronize()
+            assert torch.equal(c1, chk[s]) and torch.equal(y1, cod[s])
+
+
+def test_padded_strides():
+    """Strides larger than the minimum: bytes between stripes are left untouched."""
+    _need_gpu()
+    cfg = configs.get(2)
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    S = 3
+    D = inputs.stripe_data(cfg, num_stripes=S).numpy()
+    go = oracle.generate_graph(cfg)
+    C, Y = oracle.encode(go, D)
+    for variant in (fsb.VARIANT_SMEM, fsb.VARIANT_GLOBAL):
+        g = fsb.Graph.create(cfg)
+        g.set_variant(variant)
+        ds, cs, ys = (k + 3) * t + 16, (p + 1) * t + 32, (n + 2) * t + 48
+        dbuf = torch.zeros(S * ds, dtype=torch.uint8, device="cuda")
+        for s in range(S):
+            dbuf[s * ds:s * ds + k * t] = torch.from_numpy(D[s].reshape(-1)).cuda()
+        cbuf = torch.full((S * cs,), 0x33, dtype=torch.uint8, device="cuda")
+        ybuf = torch.full((S * ys,), 0x44, dtype=torch.uint8, device="cuda")
+        g.encode_stripes_raw(S, dbuf.data_ptr(), ds, cbuf.data_ptr(), cs, ybuf.data_ptr(), ys)
+        torch.cuda.synchronize()
+        cb, yb = cbuf.cpu().numpy(), ybuf.cpu().numpy()
+        for s in range(S):
+            _assert_equal(cb[s * cs:s * cs + p * t].reshape(p, t), C[s], "checks")
+            _assert_equal(yb[s * ys:s * ys + n * t].reshape(n, t), Y[s], "coded")
+            assert np.all(cb[s * cs + p * t:(s + 1) * cs] == 0x33)
+            assert np.all(yb[s * ys + n * t:(s + 1) * ys] == 0x44)
+
+
+EDGE_CASES = [
+    # (name, cfg, stripes)
+    ("t16_min", dict(k=37, p=3, d_p=2, n=50, t=16, dist=configs.RSD, rsd_c=0.1, rsd_delta=0.05, seed=11), 7),
+    ("t48_ragged", dict(k=64, p=5, d_p=3, n=91, t=48, dist=configs.FINITE, seed=12,
+                        fin_deg=configs.OMEGA_DEGREES, fin_prob=configs.OMEGA_PROBS), 3),
+    ("t1040_ragged", dict(k=300, p=7, d_p=4, n=400, t=1040, dist=configs.RSD, rsd_c=0.1, rsd_delta=0.05,
+                          seed=13), 2),
+    ("k1_p0", dict(k=1, p=0, d_p=0, n=33, t=256, dist=configs.FINITE, seed=14,
+                   fin_deg=configs.OMEGA_DEGREES, fin_prob=configs.OMEGA_PROBS), 4),
+    ("deg1_only", dict(k=40, p=0, d_p=0, n=90, t=128, dist=configs.FINITE, seed=15, fin_deg=(1,),
+                       fin_prob=(1.0,)), 300),
+    ("dense_rows", dict(k=70, p=10, d_p=70, n=64, t=384, dist=configs.FINITE, seed=16,
+                        fin_deg=(60, 80), fin_prob=(0.5, 0.5)), 300),
+    ("k_not_mult32_many_stripes", dict(k=333, p=40, d_p=3, n=500, t=256, dist=configs.RSD, rsd_c=0.05,
+                                       rsd_delta=0.01, seed=17), 400),
+    ("p_over_64_checks", dict(k=500, p=150, d_p=5, n=600, t=128, dist=configs.RSD, rsd_c=0.1,
+                              rsd_delta=0.05, seed=18), 320),
+]
+
+
+@pytest.mark.parametrize("name,cfg,S", EDGE_CASES, ids=[e[0] for e in EDGE_CASES])
+def test_edge_cases(name, cfg, S):
+    _need_gpu()
+    cfg = dict(cfg, stripes=S)
+    go = oracle.generate_graph(cfg)
+    D = inputs.stripe_data(cfg).numpy()
+    C, Y = oracle.encode(go, D)
+    variants = [fsb.VARIANT_AUTO, fsb.VARIANT_GLOBAL]
+    if fsb.Graph.create(cfg).info()["smem_eligible"]:
+        variants.append(fsb.VARIANT_SMEM)
+    for v in variants:
+        _, c, y = _run(cfg, v, data=torch.from_numpy(D).cuda())
+        if cfg["p"]:
+            _assert_equal(c, C, "%s checks v%d" % (name, v))
+        _assert_equal(y, Y, "%s coded v%d" % (name, v))
+
+
+def test_empty_calls_are_noops():
+    _need_gpu()
+    cfg = configs.get(1)
+    g = fsb.Graph.create(cfg)
+    d = inputs.stripe_data(cfg, device="cuda")
+    out = torch.full((4, cfg["t"]), 7, dtype=torch.uint8, device="cuda")
+    g.encode(d[0], None, out, 5, 5)                          # empty row range
+    g.encode_stripes(d[:0], None, torch.empty((0, cfg["n"], cfg["t"]), dtype=torch.uint8, device="cuda"))
+    torch.cuda.synchronize()
+    assert torch.all(out == 7)
+
+
+def test_invalid_arguments_rejected():
+    _need_gpu()
+    cfg = configs.get(2)
+    g = fsb.Graph.create(cfg)
+    d = inputs.stripe_data(cfg, device="cuda")
+    chk = torch.empty((1, cfg["p"], cfg["t"]), dtype=torch.uint8, device="cuda")
+    cod = torch.empty((1, cfg["n"], cfg["t"]), dtype=torch.uint8, device="cuda")
+    with pytest.raises(fsb.FsError):
+        g.encode(d[0], None, cod[0])                         # p > 0 needs checks
+    with pytest.raises(fsb.FsError):
+        g.encode(d[0], chk[0], cod[0], 10, 5)                # bad row range
+    with pytest.raises(fsb.FsError):
+        g.encode_stripes_raw(1, d.data_ptr() + 8, cfg["k"] * cfg["t"], chk.data_ptr(), cfg["p"] * cfg["t"],
+                             cod.data_ptr(), cfg["n"] * cfg["t"])   # misaligned
+    with pytest.raises(fsb.FsError):
+        g.encode_stripes_raw(1, d.data_ptr(), cfg["k"] * cfg["t"] - 16, chk.data_ptr(), cfg["p"] * cfg["t"],
+                             cod.data_ptr(), cfg["n"] * cfg["t"])   # stride too small
+
+
+def test_launch_counts():
+    _need_gpu()
+    cfg = configs.get(4)
+    g = fsb.Graph.create(cfg)
+    d = inputs.stripe_data(cfg, num_stripes=16, device="cuda")
+    chk = torch.empty((16, cfg["p"], cfg["t"]), dtype=torch.uint8, device="cuda")
+    cod = torch.empty((16, cfg["n"], cfg["t"]), dtype=torch.uint8, device="cuda")
+    g.set_variant(fsb.VARIANT_SMEM)
+    g.encode_stripes(d, chk, cod)
+    assert fsb.last_launch_count() == 1
+    g.set_variant(fsb.VARIANT_GLOBAL)
+    g.encode_stripes(d, chk, cod)
+    assert fsb.last_launch_count() == 2
+    torch.cuda.synchronize()
+
+
+def test_decode_gpu_output_roundtrip():
+    """P8 on the GPU's bytes: the oracle's decoder recovers the data from a random 95%
+    subset of the CUDA path's coded symbols (config 2)."""
+    _need_gpu()
+    cfg = configs.get(2)
+    _, c, y = _run(cfg, fsb.VARIANT_AUTO)
+    go = oracle.generate_graph(cfg)
+    D = inputs.stripe_data(cfg).numpy()[0]
+    recv = np.random.default_rng(3).random(cfg["n"]) < 0.95
+    I, state = oracle.decode(go, recv, y[0])
+    ok = state[:cfg["k"]] != 0
+    assert ok.sum() > 0.9 * cfg["k"]
+    assert np.array_equal(I[:cfg["k"]][ok], D[ok])
