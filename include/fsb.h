@@ -151,6 +151,14 @@ FSB_API fs_status fs_encode_stripes(const fs_graph *g, uint32_t num_stripes,
                             uint8_t *d_checks, uint64_t checks_stride,
                             uint8_t *d_coded, uint64_t coded_stride, void *stream);
 
+/* Diagnostic view of the SMEM kernel's host-built LT schedule (owned by g):
+ * words = kConsumerWarps(16) x regs x 32 uint32 words (word r*32+lane of warp w = register r of
+ * lane `lane`); step e of lane group q of warp w is the (q&1) 16-bit half of that warp's word
+ * 2e+(q>>1); values < 0x7FFF are tile-relative source rows, 0x7FFF idle, >= 0x8000 store markers.
+ * warp_steps[16] = steps per warp.  FS_EUNSUPPORTED when the graph is not SMEM-eligible.     */
+FSB_API fs_status fs_graph_schedule(const fs_graph *g, const uint32_t **words, uint32_t *regs,
+                                    const uint32_t **warp_steps, uint32_t *kpad);
+
 /* Number of kernel launches the last successful fs_encode / fs_encode_stripes on this
  * thread enqueued (for launch accounting in benchmarks).                                 */
 FSB_API uint32_t fs_last_launch_count(void);

@@ -140,7 +140,7 @@ fs_status fs_graph_get_info(const fs_graph *h, fs_graph_info *info) {
   info->variant = g.variant;
   info->smem_eligible = g.smem_eligible ? 1 : 0;
   info->smem_bytes = g.smem_bytes;
-  info->sched_bytes = static_cast<uint32_t>(g.sched.words.size() * 2);
+  info->sched_bytes = static_cast<uint32_t>(g.sched.words.size() * 4);
   info->sched_steps_max = g.sched.steps_max;
   info->sched_steps_avg = (g.sched.steps_total + fsb::kConsumerWarps / 2) / fsb::kConsumerWarps;
   info->device = g.dev.device;
@@ -215,6 +215,18 @@ fs_status fs_encode_stripes(const fs_graph *h, uint32_t S, const uint8_t *d_data
                           stream, &launches);
   if (st == FS_OK) fsb::g_launches = launches;
   return st;
+}
+
+fs_status fs_graph_schedule(const fs_graph *h, const uint32_t **words, uint32_t *regs,
+                            const uint32_t **warp_steps, uint32_t *kpad) {
+  if (!h) { set_error("null graph"); return FS_EINVAL; }
+  const fsb::Graph &g = h->g;
+  if (!g.smem_eligible || g.sched.words.empty()) { set_error("graph has no SMEM schedule"); return FS_EUNSUPPORTED; }
+  if (words) *words = g.sched.words.data();
+  if (regs) *regs = g.sched.regs;
+  if (warp_steps) *warp_steps = g.sched.warp_steps.data();
+  if (kpad) *kpad = g.sched.kpad;
+  return FS_OK;
 }
 
 uint32_t fs_last_launch_count(void) { return fsb::g_launches; }

@@ -192,24 +192,18 @@ fs_status validate_csr(const Graph &g) {
 }
 
 // ------------------------------------------------------------ SMEM kernel work schedule
-// Degree-aware, edge-balanced split of one tile's LT work over kConsumerWarps warps:
-//  * rows of degree > kSplitThreshold become "split" items: the 4 groups of a warp take
-//    every 4th edge and the partial XORs are combined with two warp shuffles;
-//  * the other rows are sorted by degree and packed 4 per item (one per 8-lane group), so
-//    the 4 groups of a warp run nearly equal edge counts in lockstep;
-//  * items are dealt to warps longest-first onto the least-loaded warp (LPT).
+// Degree-aware, edge-balanced split of one tile's LT work over kConsumerWarps warps (format:
+// SmemSchedule in fsb_internal.h).
 void build_smem_schedule(Graph &g) {
   SmemSchedule &s = g.sched;
   s = SmemSchedule();
+  g.smem_eligible = false;
   const uint32_t k = g.prm.k, p = g.prm.p, n = g.prm.n;
   s.kpad = (k + kUnitRows - 1) / kUnitRows * kUnitRows;
   s.data_units = s.kpad / kUnitRows;
   s.check_units = (p + kUnitRows - 1) / kUnitRows;
   s.tile_units = s.data_units + s.check_units;
-  if (g.prm.t % kSliceBytes != 0 || n > 65535 || s.kpad + p > 65535) {
-    g.smem_eligible = false;
-    return;
-  }
+  if (g.prm.t % kSliceBytes != 0 || n > kMaxSmemRows || s.kpad + p > kMaxSmemSlots) return;
   auto slot = [&](int32_t m) -> uint16_t {
     return static_cast<uint16_t>(static_cast<uint32_t>(m) < k ? m : s.kpad + (m - k));
   };
@@ -218,7 +212,7 @@ void build_smem_schedule(Graph &g) {
 
   struct Item {
     bool split;
-    uint32_t steps;
+    uint32_t steps;                  // edge steps (the store step comes on top)
     uint32_t rows[4];
     std::vector<uint16_t> lanes[4];  // per group, the slots of its steps
   };
@@ -229,8 +223,7 @@ void build_smem_schedule(Graph &g) {
     if (d > static_cast<uint32_t>(kSplitThreshold)) {
       Item it;
       it.split = true;
-      it.rows[0] = j;
-      it.rows[1] = it.rows[2] = it.rows[3] = kSlotNone;
+      it.rows[0] = it.rows[1] = it.rows[2] = it.rows[3] = j;
       for (uint32_t e = 0; e < d; ++e) it.lanes[e % 4].push_back(slot(g.lt_col[g.lt_row_ptr[j] + e]));
       it.steps = (d + 3) / 4;
       items.push_back(std::move(it));
@@ -252,13 +245,13 @@ void build_smem_schedule(Graph &g) {
         for (int32_t e = g.lt_row_ptr[j]; e < g.lt_row_ptr[j + 1]; ++e) it.lanes[q].push_back(slot(g.lt_col[e]));
         it.steps = std::max<uint32_t>(it.steps, static_cast<uint32_t>(it.lanes[q].size()));
       } else {
-        it.rows[q] = kSlotNone;
+        it.rows[q] = UINT32_MAX;
       }
     }
     items.push_back(std::move(it));
   }
-  // LPT over warps; cost = steps + per-item overhead (header, store, shuffles)
-  auto cost = [](const Item &it) { return it.steps + (it.split ? 3u : 2u); };
+  // LPT over warps; cost = edge steps + the store step (+1 for the split shuffles)
+  auto cost = [](const Item &it) { return it.steps + (it.split ? 2u : 1u); };
   std::vector<uint32_t> order(items.size());
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost(items[a]) > cost(items[b]); });
@@ -266,39 +259,49 @@ void build_smem_schedule(Graph &g) {
   std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
   for (int w = 0; w < kConsumerWarps; ++w) heap.push({0, w});
   std::vector<std::vector<uint32_t>> per_warp(kConsumerWarps);
-  std::vector<uint64_t> warp_steps(kConsumerWarps, 0);
   for (uint32_t idx : order) {
     Load l = heap.top();
     heap.pop();
     per_warp[l.second].push_back(idx);
-    warp_steps[l.second] += items[idx].steps;
     heap.push({l.first + cost(items[idx]), l.second});
   }
-  // encode
-  s.warp_begin.assign(kConsumerWarps + 1, 0);
+  // per-warp step streams: [steps x 4 values] per item, then its store step
+  std::vector<std::vector<uint16_t>> streams(kConsumerWarps);
+  s.warp_steps.assign(kConsumerWarps, 0);
+  s.steps_max = s.steps_total = 0;
   for (int w = 0; w < kConsumerWarps; ++w) {
-    s.warp_begin[w] = static_cast<uint32_t>(s.words.size() / 8);
+    std::vector<uint16_t> &st = streams[w];
     for (uint32_t idx : per_warp[w]) {
       const Item &it = items[idx];
-      uint16_t hdr[8] = {static_cast<uint16_t>(it.steps), static_cast<uint16_t>(it.split ? 1 : 0),
-                         static_cast<uint16_t>(it.rows[0]), static_cast<uint16_t>(it.rows[1]),
-                         static_cast<uint16_t>(it.rows[2]), static_cast<uint16_t>(it.rows[3]), 0, 0};
-      s.words.insert(s.words.end(), hdr, hdr + 8);
-      const uint32_t chunks = (it.steps + 7) / 8;
-      for (uint32_t c = 0; c < chunks; ++c)
-        for (int q = 0; q < 4; ++q)
-          for (int u = 0; u < 8; ++u) {
-            const uint32_t st = c * 8 + u;
-            s.words.push_back(st < it.lanes[q].size() ? it.lanes[q][st] : kSlotNone);
-          }
+      for (uint32_t e = 0; e < it.steps; ++e)
+        for (int q = 0; q < 4; ++q) st.push_back(e < it.lanes[q].size() ? it.lanes[q][e] : kIdle);
+      for (int q = 0; q < 4; ++q) {
+        uint16_t v;
+        if (it.split) v = static_cast<uint16_t>(kStoreFlag | kSplitFlag | it.rows[0]);
+        else if (it.rows[q] == UINT32_MAX) v = kStoreNone;
+        else v = static_cast<uint16_t>(kStoreFlag | it.rows[q]);
+        st.push_back(v);
+      }
     }
+    s.warp_steps[w] = static_cast<uint32_t>(st.size() / 4);
+    s.steps_max = std::max(s.steps_max, s.warp_steps[w]);
+    s.steps_total += s.warp_steps[w];
   }
-  s.warp_begin[kConsumerWarps] = static_cast<uint32_t>(s.words.size() / 8);
-  s.steps_max = 0;
-  s.steps_total = 0;
+  if (s.steps_max > kMaxWarpSteps) return;  // too much work per tile for the register schedule
+  s.regs = s.steps_max <= 16u * kStepsPerReg ? 16 : kSchedRegsMax;
+  // word layout per warp: word (r*32 + lane) = register r of lane `lane`; step e, group q is
+  // the (q&1) half of stream word 2e + (q>>1) -> register (2e+(q>>1))/32, lane (2e+(q>>1))%32
+  const uint32_t wpw = s.regs * 32;
+  s.words.assign(static_cast<size_t>(kConsumerWarps) * wpw, (static_cast<uint32_t>(kIdle) << 16) | kIdle);
   for (int w = 0; w < kConsumerWarps; ++w) {
-    s.steps_max = std::max<uint32_t>(s.steps_max, static_cast<uint32_t>(warp_steps[w]));
-    s.steps_total += static_cast<uint32_t>(warp_steps[w]);
+    const std::vector<uint16_t> &st = streams[w];
+    for (size_t e = 0; e < st.size() / 4; ++e)
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t word = static_cast<uint32_t>(2 * e + (q >> 1));
+        uint32_t &dst = s.words[static_cast<size_t>(w) * wpw + word];
+        const uint32_t v = st[e * 4 + q];
+        dst = (q & 1) ? ((dst & 0x0000FFFFu) | (v << 16)) : ((dst & 0xFFFF0000u) | v);
+      }
   }
   g.smem_eligible = true;
 }

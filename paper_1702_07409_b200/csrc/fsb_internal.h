@@ -18,20 +18,36 @@ constexpr int kConsumerWarps = 16;
 constexpr int kGroupsPerWarp = 4;                        // 8 lanes x 16 B = one 128-B row
 constexpr int kGroups = kConsumerWarps * kGroupsPerWarp;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;      // + 1 TMA producer warp
-constexpr uint16_t kSlotNone = 0xFFFF;
 constexpr int kSplitThreshold = 32;                      // rows of degree > this are split
                                                          // over the 4 groups of a warp
+// Register-resident schedule: each warp keeps its whole per-tile step stream in registers
+// (kSchedRegsMax 32-bit words per lane = 16 steps per word) and fetches step e of its lane
+// group with one warp shuffle.
+constexpr int kStepsPerReg = 16;
+constexpr int kSchedRegsMax = 32;
+constexpr uint32_t kMaxWarpSteps = kStepsPerReg * kSchedRegsMax;
+// 16-bit step values (one per lane group and step):
+constexpr uint16_t kIdle = 0x7FFF;        // no edge this step (row shorter than the item)
+constexpr uint16_t kStoreFlag = 0x8000;   // store step: 0x8000 | row  (row < 0x4000)
+constexpr uint16_t kSplitFlag = 0x4000;   //   split item: 0xC000 | row in all four groups
+constexpr uint16_t kStoreNone = 0xBFFF;   //   store step, nothing to store (row 0x3FFF; no split bit)
+constexpr uint32_t kMaxSmemRows = 0x3FFF; // n limit of the SMEM variant (rows 0..0x3FFE)
+constexpr uint32_t kMaxSmemSlots = 0x7FFE;
 
 // Host-built LT work schedule of the SMEM kernel (identical for every tile).
-// Per warp, a run of items.  Item = 16-B header {steps, flags, row0..row3, 0, 0} followed by
-// ceil(steps/8) chunks; chunk c = 4 groups x 8 uint16 slots (steps 8c..8c+7 of group g at
-// bytes 16*g..16*g+15).  A slot is a tile-relative row (data m -> m, check i -> kpad+i);
-// kSlotNone = no edge.  flags bit0 = split item (one row, edges dealt over the 4 groups,
-// combined by warp shuffles).
+// Rows of degree > kSplitThreshold are "split" items: their edges are dealt over the 4
+// lane groups of a warp and the partial XORs combined with two warp shuffles.  Other rows
+// are sorted by degree and packed 4 per item (one per 8-lane group) so the groups of a warp
+// run nearly equal edge counts in lockstep.  Items are dealt to warps longest-first onto
+// the least-loaded warp (LPT).  Each warp's stream is a sequence of steps; a step holds one
+// 16-bit value per group: a tile-relative source row (data m -> m, check i -> kpad+i), kIdle,
+// or (after an item's last edge) a store marker.  Stored as 32-bit words: step e, group g
+// is the (g&1) half of word 2e + (g>>1) of the warp's stream (see fsb_smem_encode).
 struct SmemSchedule {
-  std::vector<uint16_t> words;          // items of all warps, 16-B aligned
-  std::vector<uint32_t> warp_begin;     // kConsumerWarps+1 offsets, in 16-B units
+  std::vector<uint32_t> words;          // kConsumerWarps x (regs*32) words
+  std::vector<uint32_t> warp_steps;     // steps per warp (incl. store steps)
   std::vector<uint16_t> pre_slots;      // p * d_p tile-relative data rows
+  uint32_t regs = 0;                    // 32-bit schedule registers per lane (16 or 32)
   uint32_t kpad = 0;                    // data rows rounded up to kUnitRows
   uint32_t data_units = 0, check_units = 0, tile_units = 0;
   uint32_t steps_max = 0, steps_total = 0;
@@ -40,8 +56,8 @@ struct SmemSchedule {
 struct DeviceBufs {
   int device = -1;
   int32_t *pre_row_ptr = nullptr, *pre_col = nullptr, *lt_row_ptr = nullptr, *lt_col = nullptr;
-  uint16_t *sched = nullptr;
-  uint32_t *warp_begin = nullptr;
+  uint32_t *sched = nullptr;
+  uint32_t *warp_steps = nullptr;
   uint16_t *pre_slots = nullptr;
 };
 

@@ -92,8 +92,8 @@ __device__ __forceinline__ void st_stream(uint8_t *p, const uint4 &v) {
 
 // ============================================================================ SMEM kernel
 struct SmemArgs {
-  const uint16_t *sched;       // items (16-B units)
-  const uint32_t *warp_begin;  // kConsumerWarps + 1
+  const uint32_t *sched;       // kConsumerWarps x (NR*32) schedule words
+  const uint32_t *warp_steps;  // kConsumerWarps
   const uint16_t *pre_slots;   // p * d_p
   uint8_t *checks;
   uint64_t checks_stride;
@@ -109,6 +109,23 @@ __device__ __forceinline__ uint32_t unit_use(uint32_t x, uint32_t i, uint32_t T,
   return (in_even && in_odd) ? i : (i >> 1);
 }
 
+template <int NR>
+__device__ __forceinline__ void store_item(uint4 acc, uint32_t v, uint32_t grp, uint8_t *out, uint64_t t) {
+  if (v & kSplitFlag) {  // split row: combine the four groups' partial XORs (uniform branch)
+#pragma unroll
+    for (int o = 8; o <= 16; o <<= 1) {
+      acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, o);
+      acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, o);
+      acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, o);
+    }
+    if (grp == 0) st_stream(out + static_cast<uint64_t>(v & 0x3FFF) * t, acc);
+  } else if ((v & 0x3FFF) != 0x3FFF) {
+    st_stream(out + static_cast<uint64_t>(v & 0x3FFF) * t, acc);
+  }
+}
+
+template <int NR>
 __global__ void __launch_bounds__(kThreads, 1)
     fsb_smem_encode(const __grid_constant__ CUtensorMap tmap, const SmemArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -162,8 +179,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint4 *ring4w = reinterpret_cast<uint4 *>(smem);
   const uint32_t grp = lane >> 3, lane8 = lane & 7;
   const uint32_t gidx = warp * kGroupsPerWarp + grp;
-  const uint4 *sched = reinterpret_cast<const uint4 *>(a.sched);
-  const uint32_t w_begin = __ldg(&a.warp_begin[warp]), w_end = __ldg(&a.warp_begin[warp + 1]);
+  // this warp's whole LT schedule lives in registers for the kernel's lifetime
+  uint32_t R[NR];
+  {
+    const uint32_t *sw = a.sched + static_cast<size_t>(warp) * (NR * 32);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) R[r] = __ldg(&sw[r * 32 + lane]);
+  }
+  const uint32_t nsteps = __ldg(&a.warp_steps[warp]);
+  const uint32_t src_hi = grp >> 1, sh = (grp & 1) * 16;
   uint32_t i = 0;
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
     const uint32_t stripe = tile / a.nslices, slice = tile % a.nslices;
@@ -189,40 +213,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       consumer_bar();
     }
 
-    // (2) LT rows (PAPER.md:91 step (2)) from the schedule
+    // (2) LT rows (PAPER.md:91 step (2)): step e of group grp is a warp shuffle away
     uint8_t *out = a.coded + stripe * a.coded_stride + col_off;
-    for (uint32_t it = w_begin; it < w_end;) {
-      const uint4 hdr = __ldg(&sched[it]);
-      const uint32_t steps = hdr.x & 0xFFFF, split = hdr.x >> 16;
-      const uint32_t nchunks = (steps + 7) >> 3;
-      const uint4 *ch = sched + it + 1 + grp;
-      uint4 acc = make_uint4(0, 0, 0, 0);
-      for (uint32_t c = 0; c < nchunks; ++c) {
-        const uint4 sl = __ldg(&ch[c * 4]);
-        const uint32_t w[4] = {sl.x, sl.y, sl.z, sl.w};
+    uint4 acc = make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t s0 = w[q] & 0xFFFF, s1 = w[q] >> 16;
-          if (s0 != kSlotNone) xor_into(acc, ring4[tbase + s0 * 8]);
-          if (s1 != kSlotNone) xor_into(acc, ring4[tbase + s1 * 8]);
+    for (int r = 0; r < NR; ++r) {
+      if (static_cast<uint32_t>(r) * kStepsPerReg >= nsteps) break;
+      const uint32_t reg = R[r];
+      for (uint32_t q = 0; q < static_cast<uint32_t>(kStepsPerReg); q += 4) {
+        if (r * kStepsPerReg + q >= nsteps) break;
+        uint32_t v[4];
+        uint4 x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = (__shfl_sync(0xffffffffu, reg, 2 * (q + j) + src_hi) >> sh) & 0xFFFF;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          x[j] = make_uint4(0, 0, 0, 0);
+          if (v[j] < kIdle) x[j] = ring4[tbase + v[j] * 8];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (v[j] & kStoreFlag) {  // store step: the same for every group of the warp
+            store_item<NR>(acc, v[j], grp, out, a.t);
+            acc = make_uint4(0, 0, 0, 0);
+          } else {
+            xor_into(acc, x[j]);
+          }
         }
       }
-      uint32_t row;
-      if (split) {
-#pragma unroll
-        for (int o = 8; o <= 16; o <<= 1) {
-          acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, o);
-          acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, o);
-          acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, o);
-          acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, o);
-        }
-        row = (grp == 0) ? (hdr.y & 0xFFFF) : kSlotNone;
-      } else {
-        const uint32_t rw = (grp < 2) ? hdr.y : hdr.z;
-        row = (grp & 1) ? (rw >> 16) : (rw & 0xFFFF);
-      }
-      if (row != kSlotNone) st_stream(out + static_cast<uint64_t>(row) * a.t, acc);
-      it += 1 + nchunks * 4;
     }
     // release the tile's units to the producer
     fence_proxy_async_smem();
@@ -351,7 +369,7 @@ void free_device(Graph &g) {
   cudaFree(d.lt_row_ptr);
   cudaFree(d.lt_col);
   cudaFree(d.sched);
-  cudaFree(d.warp_begin);
+  cudaFree(d.warp_steps);
   cudaFree(d.pre_slots);
   if (prev >= 0) cudaSetDevice(prev);
   d = DeviceBufs();
@@ -381,10 +399,13 @@ fs_status upload_graph(Graph &g) {
       g.smem_eligible = false;
     } else {
       if ((st = upload(&g.dev.sched, g.sched.words.data(), g.sched.words.size())) != FS_OK) return st;
-      if ((st = upload(&g.dev.warp_begin, g.sched.warp_begin.data(), g.sched.warp_begin.size())) != FS_OK) return st;
+      if ((st = upload(&g.dev.warp_steps, g.sched.warp_steps.data(), g.sched.warp_steps.size())) != FS_OK) return st;
       if ((st = upload(&g.dev.pre_slots, g.sched.pre_slots.data(), g.sched.pre_slots.size())) != FS_OK) return st;
-      e = cudaFuncSetAttribute(fsb_smem_encode, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(fsb_smem_encode<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(g.smem_bytes));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fsb_smem_encode<kSchedRegsMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(g.smem_bytes));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     }
   }
@@ -428,7 +449,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     }
     SmemArgs a;
     a.sched = g.dev.sched;
-    a.warp_begin = g.dev.warp_begin;
+    a.warp_steps = g.dev.warp_steps;
     a.pre_slots = g.dev.pre_slots;
     a.checks = checks;
     a.checks_stride = checks_stride;
@@ -444,7 +465,10 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     a.tile_units = g.sched.tile_units;
     a.ring_units = g.ring_units;
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, g.sm_count));
-    fsb_smem_encode<<<grid, kThreads, g.smem_bytes, stream>>>(tmap, a);
+    if (g.sched.regs <= 16)
+      fsb_smem_encode<16><<<grid, kThreads, g.smem_bytes, stream>>>(tmap, a);
+    else
+      fsb_smem_encode<kSchedRegsMax><<<grid, kThreads, g.smem_bytes, stream>>>(tmap, a);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_smem_encode launch");
     *launches = 1;
     return FS_OK;

@@ -147,3 +147,57 @@ def test_schedule_balance():
         assert inf["smem_eligible"] == 1
         assert inf["sched_steps_avg"] * 16 >= inf["lt_nnz"] // 4
         assert inf["sched_steps_max"] <= 1.05 * inf["sched_steps_avg"] + 4
+
+
+def _simulate_schedule(g, c):
+    """Replays the SMEM kernel's consumption of its register schedule (fsb_smem_encode) on
+    the host: returns {row: sorted tile-relative slots} and asserts store steps are
+    warp-uniform (the kernel's shuffles rely on it)."""
+    words, steps, kpad = g.schedule()
+    rows = {}
+    for w in range(16):
+        flat = words[w].reshape(-1)            # word index = r*32 + lane
+        acc = [[] for _ in range(4)]
+        for e in range(int(steps[w])):
+            vals = []
+            for q in range(4):
+                word = int(flat[2 * e + (q >> 1)])
+                vals.append((word >> (16 * (q & 1))) & 0xFFFF)
+            stores = [v >= 0x8000 for v in vals]
+            assert all(stores) or not any(stores), "non-uniform store step"
+            if all(stores):
+                splits = [bool(v & 0x4000) for v in vals]
+                assert all(splits) or not any(splits), "non-uniform split flag"
+                if all(splits):
+                    assert len(set(vals)) == 1
+                    row = vals[0] & 0x3FFF
+                    assert row not in rows
+                    rows[row] = sorted(sum(acc, []))
+                else:
+                    for q in range(4):
+                        row = vals[q] & 0x3FFF
+                        if row != 0x3FFF:
+                            assert row not in rows
+                            rows[row] = sorted(acc[q])
+                acc = [[] for _ in range(4)]
+            else:
+                for q in range(4):
+                    if vals[q] < 0x7FFF:
+                        acc[q].append(vals[q])
+        assert not any(acc), "edges after the last store step"
+        rest = flat[2 * int(steps[w]):]
+        assert np.all(rest == 0x7FFF7FFF)
+    return rows, kpad
+
+
+@pytest.mark.parametrize("cid", [1, 2, 4])
+def test_smem_schedule_covers_every_edge(cid):
+    c = configs.get(cid)
+    g = fsb.Graph.create(c, host_only=True)
+    rows, kpad = _simulate_schedule(g, c)
+    _, _, lt_rp, lt_c = g.csr()
+    assert sorted(rows) == list(range(c["n"]))
+    k = c["k"]
+    for j in range(c["n"]):
+        want = sorted(m if m < k else kpad + (m - k) for m in lt_c[lt_rp[j]:lt_rp[j + 1]])
+        assert rows[j] == want
