@@ -124,15 +124,16 @@ typedef struct {
   int32_t smem_eligible;     /* 1 when the SMEM variant can run this graph                    */
   uint32_t smem_bytes;       /* dynamic shared memory of the SMEM kernel                      */
   uint32_t sched_bytes;      /* size of the SMEM kernel's work schedule                       */
-  uint32_t sched_steps_max;  /* SMEM schedule: steps of the most loaded warp per tile         */
-  uint32_t sched_steps_avg;  /* SMEM schedule: mean steps per warp per tile (x1, rounded)     */
+  uint32_t sched_steps_max;  /* SMEM schedule: gather slots of the most loaded warp per tile  */
+  uint32_t sched_steps_avg;  /* SMEM schedule: mean gather slots per warp per tile (rounded)  */
   int32_t device;            /* CUDA device of the device copy, -1 for host-only graphs       */
 } fs_graph_info;
 
 FSB_API fs_status fs_graph_get_info(const fs_graph *g, fs_graph_info *info);
 
 /* Force a kernel variant (FS_VARIANT_*).  FS_EUNSUPPORTED if SMEM is requested for a graph
- * that is not eligible (t % 128 != 0, n > 65535 or the tile does not fit shared memory). */
+ * that is not eligible (t % 64 != 0, n > 65534, K+2 > 2047 tile rows, or two 64-B tiles plus
+ * the schedule do not fit shared memory).                                                                */
 FSB_API fs_status fs_graph_set_variant(fs_graph *g, int32_t variant);
 
 /* One stripe, coded rows [row_begin, row_end) (row partition across GPUs).
@@ -151,13 +152,19 @@ FSB_API fs_status fs_encode_stripes(const fs_graph *g, uint32_t num_stripes,
                             uint8_t *d_checks, uint64_t checks_stride,
                             uint8_t *d_coded, uint64_t coded_stride, void *stream);
 
-/* Diagnostic view of the SMEM kernel's host-built LT schedule (owned by g; see DESIGN.md §5):
- * words = kConsumerWarps(16) x regs x 32 uint32 words (word r*32+lane of warp w = register r of
- * lane `lane`); step e of lane group q of warp w is the (q&1) 16-bit half of that warp's word
- * 2e+(q>>1); values < 0x7FFF are tile-relative source rows, 0x7FFF idle, >= 0x8000 store markers.
- * warp_steps[16] = steps per warp.  FS_EUNSUPPORTED when the graph is not SMEM-eligible.     */
-FSB_API fs_status fs_graph_schedule(const fs_graph *g, const uint32_t **words, uint32_t *regs,
-                                    const uint32_t **warp_steps, uint32_t *kpad);
+/* Diagnostic view of the SMEM kernel's host-built LT schedule (owned by g; DESIGN.md §5.1):
+ * words[nwords] = two chunk streams of uint32 words, the heads stream first and the conts stream
+ * from chunk cont_base on (chunk c = words 32c..32c+31; half-group h's 4 words at 32c+4h; half-
+ * group h = lanes 4h..4h+3 of a warp, h = 2*group + half).  warp_info[16*3] = {items, first head
+ * chunk, first cont chunk} per consumer warp.  A slot is an 11-bit tile row (data m -> m, check i
+ * -> kpad+i, padding -> zero_even or zero_even+1); a slot word packs two slots as a | b << 21.
+ * An item's head chunk holds, per half-group, word 0 = row | ctrl << 16 (ctrl = L | split << 15;
+ * row 0xFFFF = no output) and slots 0..5 in words 1..3; slots 6..L-1 follow in the conts stream,
+ * 8 per chunk.  In every step, half 0 of a group reads an even row iff half 1 reads an odd one
+ * (shared-memory bank rule).  FS_EUNSUPPORTED when the graph is not SMEM-eligible.          */
+FSB_API fs_status fs_graph_schedule(const fs_graph *g, const uint32_t **words, uint64_t *nwords,
+                                    uint32_t *cont_base, const uint32_t **warp_info, uint32_t *kpad,
+                                    uint32_t *zero_even);
 
 /* Number of kernel launches the last successful fs_encode / fs_encode_stripes on this
  * thread enqueued (for launch accounting in benchmarks).                                 */

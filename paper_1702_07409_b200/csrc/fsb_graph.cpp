@@ -192,30 +192,76 @@ fs_status validate_csr(const Graph &g) {
 }
 
 // ------------------------------------------------------------ SMEM kernel work schedule
-// Degree-aware, edge-balanced split of one tile's LT work over kConsumerWarps warps (format:
-// SmemSchedule in fsb_internal.h).
+// Degree-aware, edge-balanced, bank-conflict-free split of one tile's LT work over
+// kConsumerWarps warps (record format and bank rule: fsb_internal.h).
+//
+// - Rows of degree > kSplitThreshold become split items: their even tile rows are dealt
+//   round-robin to the 4 half-0 half-groups and their odd rows to the 4 half-1 half-groups.
+// - Lighter rows are paired (A for half 0, B for half 1 of one group): within a degree class,
+//   rows are sorted by their number of even sources and the most-even row is paired with the
+//   least-even one, so that A's evens meet B's odds and A's odds meet B's evens; leftovers are
+//   matched with the zero row of the opposite parity.  Pairs are sorted by length and packed
+//   4 per item (the item length is the longest pair's; shorter pairs pad with zero rows).
+// - Items are dealt longest-first to the least loaded warp (LPT).
 void build_smem_schedule(Graph &g) {
   SmemSchedule &s = g.sched;
   s = SmemSchedule();
   g.smem_eligible = false;
   const uint32_t k = g.prm.k, p = g.prm.p, n = g.prm.n;
   s.kpad = (k + kUnitRows - 1) / kUnitRows * kUnitRows;
+  s.zero_even = (s.kpad + p + 1) & ~1u;
+  s.tile_rows = s.zero_even + 2;
   s.data_units = s.kpad / kUnitRows;
-  s.check_units = (p + kUnitRows - 1) / kUnitRows;
-  s.tile_units = s.data_units + s.check_units;
-  if (g.prm.t % kSliceBytes != 0 || n > kMaxSmemRows || s.kpad + p > kMaxSmemSlots) return;
+  s.tile_units = (s.tile_rows + kUnitRows - 1) / kUnitRows;
+  if (g.prm.t % kSliceBytes != 0 || n > kMaxSmemRows || s.tile_rows > kMaxSmemSlots) return;
+  const uint16_t z0 = static_cast<uint16_t>(s.zero_even), z1 = static_cast<uint16_t>(s.zero_even + 1);
   auto slot = [&](int32_t m) -> uint16_t {
-    return static_cast<uint16_t>(static_cast<uint32_t>(m) < k ? m : s.kpad + (m - k));
+    const uint32_t r = static_cast<uint32_t>(m) < k ? static_cast<uint32_t>(m) : s.kpad + (m - k);
+    return static_cast<uint16_t>(r);
   };
   s.pre_slots.resize(g.pre_col.size());
-  for (size_t e = 0; e < g.pre_col.size(); ++e) s.pre_slots[e] = slot(g.pre_col[e]);
+  for (size_t e = 0; e < g.pre_col.size(); ++e) s.pre_slots[e] = static_cast<uint16_t>(g.pre_col[e]);
 
-  struct Item {
-    bool split;
-    uint32_t steps;                  // edge steps (the store step comes on top)
-    uint32_t rows[4];
-    std::vector<uint16_t> lanes[4];  // per group, the slots of its steps
+  struct Pair {                      // one group: half 0 (A) and half 1 (B)
+    uint16_t row[2] = {kNoRow, kNoRow};
+    std::vector<uint16_t> seq[2];    // seq[0][e] even <=> seq[1][e] odd
   };
+  struct Item {
+    bool split = false;
+    uint32_t len = 0;
+    Pair grp[4];
+  };
+  auto row_slots = [&](uint32_t j, std::vector<uint16_t> &ev, std::vector<uint16_t> &od) {
+    for (int32_t e = g.lt_row_ptr[j]; e < g.lt_row_ptr[j + 1]; ++e) {
+      const uint16_t v = slot(g.lt_col[e]);
+      ((v & 1) ? od : ev).push_back(v);
+    }
+  };
+  // pair rows A (half 0) and B (half 1; kNoRow = none) with parity-complementary steps
+  auto make_pair = [&](uint32_t a, uint32_t b) {
+    Pair pr;
+    std::vector<uint16_t> ea, oa, eb, ob;
+    row_slots(a, ea, oa);
+    pr.row[0] = static_cast<uint16_t>(a);
+    if (b != UINT32_MAX) {
+      row_slots(b, eb, ob);
+      pr.row[1] = static_cast<uint16_t>(b);
+    }
+    auto step = [&](uint16_t x, uint16_t y) {
+      pr.seq[0].push_back(x);
+      pr.seq[1].push_back(y);
+    };
+    size_t i = 0, j = 0;
+    for (; i < ea.size() && j < ob.size(); ++i, ++j) step(ea[i], ob[j]);
+    for (; i < ea.size(); ++i) step(ea[i], z1);
+    size_t u = 0, v = 0;
+    for (; u < oa.size() && v < eb.size(); ++u, ++v) step(oa[u], eb[v]);
+    for (; u < oa.size(); ++u) step(oa[u], z0);
+    for (; j < ob.size(); ++j) step(z0, ob[j]);
+    for (; v < eb.size(); ++v) step(z1, eb[v]);
+    return pr;
+  };
+
   std::vector<Item> items;
   std::vector<uint32_t> light;
   for (uint32_t j = 0; j < n; ++j) {
@@ -223,35 +269,74 @@ void build_smem_schedule(Graph &g) {
     if (d > static_cast<uint32_t>(kSplitThreshold)) {
       Item it;
       it.split = true;
-      it.rows[0] = it.rows[1] = it.rows[2] = it.rows[3] = j;
-      for (uint32_t e = 0; e < d; ++e) it.lanes[e % 4].push_back(slot(g.lt_col[g.lt_row_ptr[j] + e]));
-      it.steps = (d + 3) / 4;
+      std::vector<uint16_t> ev, od;
+      row_slots(j, ev, od);
+      for (int q = 0; q < 4; ++q) {
+        it.grp[q].row[0] = it.grp[q].row[1] = static_cast<uint16_t>(j);
+        for (size_t e = q; e < ev.size(); e += 4) it.grp[q].seq[0].push_back(ev[e]);
+        for (size_t e = q; e < od.size(); e += 4) it.grp[q].seq[1].push_back(od[e]);
+      }
+      for (int q = 0; q < 4; ++q) {
+        it.len = std::max<uint32_t>(it.len, static_cast<uint32_t>(
+                                                std::max(it.grp[q].seq[0].size(), it.grp[q].seq[1].size())));
+      }
+      for (int q = 0; q < 4; ++q) {
+        it.grp[q].seq[0].resize(it.len, z0);
+        it.grp[q].seq[1].resize(it.len, z1);
+      }
       items.push_back(std::move(it));
     } else {
       light.push_back(j);
     }
   }
+  // degree classes, each sorted by its rows' number of even sources; pair extremes
+  auto degree = [&](uint32_t j) { return static_cast<uint32_t>(g.lt_row_ptr[j + 1] - g.lt_row_ptr[j]); };
+  auto evens = [&](uint32_t j) {
+    uint32_t c = 0;
+    for (int32_t e = g.lt_row_ptr[j]; e < g.lt_row_ptr[j + 1]; ++e) c += (slot(g.lt_col[e]) & 1) ? 0 : 1;
+    return c;
+  };
+  std::vector<uint32_t> ecount(n, 0);
+  for (uint32_t j : light) ecount[j] = evens(j);
   std::stable_sort(light.begin(), light.end(), [&](uint32_t a, uint32_t b) {
-    return (g.lt_row_ptr[a + 1] - g.lt_row_ptr[a]) > (g.lt_row_ptr[b + 1] - g.lt_row_ptr[b]);
+    if (degree(a) != degree(b)) return degree(a) > degree(b);
+    return ecount[a] < ecount[b];
   });
-  for (size_t i = 0; i < light.size(); i += 4) {
+  std::vector<Pair> pairs;
+  uint32_t carry = UINT32_MAX;  // an unpaired row left over from the previous class
+  for (size_t c0 = 0; c0 < light.size();) {
+    size_t c1 = c0;
+    while (c1 < light.size() && degree(light[c1]) == degree(light[c0])) ++c1;
+    std::vector<uint32_t> cls(light.begin() + c0, light.begin() + c1);
+    if (carry != UINT32_MAX) cls.insert(cls.begin(), carry), carry = UINT32_MAX;
+    size_t lo = 0, hi = cls.size();
+    while (hi - lo >= 2) {
+      pairs.push_back(make_pair(cls[lo], cls[hi - 1]));
+      ++lo;
+      --hi;
+    }
+    if (hi - lo == 1) carry = cls[lo];
+    c0 = c1;
+  }
+  if (carry != UINT32_MAX) pairs.push_back(make_pair(carry, UINT32_MAX));
+  std::stable_sort(pairs.begin(), pairs.end(),
+                   [](const Pair &a, const Pair &b) { return a.seq[0].size() > b.seq[0].size(); });
+  for (size_t i = 0; i < pairs.size(); i += 4) {
     Item it;
-    it.split = false;
-    it.steps = 0;
+    for (int q = 0; q < 4 && i + q < pairs.size(); ++q) {
+      it.grp[q] = pairs[i + q];
+      it.len = std::max<uint32_t>(it.len, static_cast<uint32_t>(it.grp[q].seq[0].size()));
+    }
     for (int q = 0; q < 4; ++q) {
-      if (i + q < light.size()) {
-        const uint32_t j = light[i + q];
-        it.rows[q] = j;
-        for (int32_t e = g.lt_row_ptr[j]; e < g.lt_row_ptr[j + 1]; ++e) it.lanes[q].push_back(slot(g.lt_col[e]));
-        it.steps = std::max<uint32_t>(it.steps, static_cast<uint32_t>(it.lanes[q].size()));
-      } else {
-        it.rows[q] = UINT32_MAX;
-      }
+      it.grp[q].seq[0].resize(it.len, z0);
+      it.grp[q].seq[1].resize(it.len, z1);
     }
     items.push_back(std::move(it));
   }
-  // LPT over warps; cost = edge steps + the store step (+1 for the split shuffles)
-  auto cost = [](const Item &it) { return it.steps + (it.split ? 2u : 1u); };
+  for (const Item &it : items)
+    if (it.len > kMaxItemLen || it.len == 0) return;
+  // LPT over warps; cost ~ gather steps + per-item overhead (head, dispatch, store)
+  auto cost = [](const Item &it) { return it.len + (it.split ? 8u : 6u); };
   std::vector<uint32_t> order(items.size());
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost(items[a]) > cost(items[b]); });
@@ -265,44 +350,62 @@ void build_smem_schedule(Graph &g) {
     per_warp[l.second].push_back(idx);
     heap.push({l.first + cost(items[idx]), l.second});
   }
-  // per-warp step streams: [steps x 4 values] per item, then its store step
-  std::vector<std::vector<uint16_t>> streams(kConsumerWarps);
-  s.warp_steps.assign(kConsumerWarps, 0);
-  s.steps_max = s.steps_total = 0;
+  // emit the two chunk streams, warp after warp (32 words per chunk; half-group h: words 4h..4h+3)
+  s.warp_info.assign(kConsumerWarps * 3, 0);
+  std::vector<uint32_t> heads, conts;
+  auto put = [](uint32_t &word, uint32_t i, uint16_t v) {  // slot i of a word pair position
+    const uint32_t sh = (i & 1) ? kSlotHiShift : 0;
+    word = (word & ~(((1u << kSlotBits) - 1) << sh)) | (static_cast<uint32_t>(v) << sh);
+  };
+  const uint32_t wpc = kChunkBytes / 4;  // words per chunk
+  s.steps_max = s.steps_total = s.pad_slots = 0;
   for (int w = 0; w < kConsumerWarps; ++w) {
-    std::vector<uint16_t> &st = streams[w];
+    s.warp_info[w * 3 + 0] = static_cast<uint32_t>(per_warp[w].size());
+    s.warp_info[w * 3 + 1] = static_cast<uint32_t>(heads.size() / wpc);
+    s.warp_info[w * 3 + 2] = static_cast<uint32_t>(conts.size() / wpc);
+    uint32_t steps = 0;
     for (uint32_t idx : per_warp[w]) {
       const Item &it = items[idx];
-      for (uint32_t e = 0; e < it.steps; ++e)
-        for (int q = 0; q < 4; ++q) st.push_back(e < it.lanes[q].size() ? it.lanes[q][e] : kIdle);
-      for (int q = 0; q < 4; ++q) {
-        uint16_t v;
-        if (it.split) v = static_cast<uint16_t>(kStoreFlag | kSplitFlag | it.rows[0]);
-        else if (it.rows[q] == UINT32_MAX) v = kStoreNone;
-        else v = static_cast<uint16_t>(kStoreFlag | it.rows[q]);
-        st.push_back(v);
+      const size_t hb = heads.size();
+      heads.resize(hb + wpc, 0);
+      const uint32_t ncont = it.len > kHeadSlots ? (it.len - kHeadSlots + kChunkSlots - 1) / kChunkSlots : 0;
+      const size_t cb = conts.size();
+      conts.resize(cb + static_cast<size_t>(ncont) * wpc, 0);
+      for (int h = 0; h < kHalvesPerWarp; ++h) {
+        const Pair &pr = it.grp[h >> 1];
+        const std::vector<uint16_t> &seq = pr.seq[h & 1];
+        heads[hb + h * 4] = static_cast<uint32_t>(pr.row[h & 1]) |
+                            (static_cast<uint32_t>(it.len | (it.split ? kSplitBit : 0)) << 16);
+        for (uint32_t e = 0; e < it.len; ++e) {
+          if (seq[e] == z0 || seq[e] == z1) ++s.pad_slots;
+          if (e < kHeadSlots) {
+            put(heads[hb + h * 4 + 1 + e / 2], e, seq[e]);
+          } else {
+            const uint32_t f = e - kHeadSlots;
+            put(conts[cb + (f / kChunkSlots) * wpc + h * 4 + (f % kChunkSlots) / 2], f, seq[e]);
+          }
+        }
+        // unused slot positions of the last chunk: parity-correct zero rows (never read)
+        const uint16_t zp = (h & 1) ? z1 : z0;
+        for (uint32_t e = it.len; e < kHeadSlots + ncont * kChunkSlots; ++e) {
+          if (e < kHeadSlots) {
+            put(heads[hb + h * 4 + 1 + e / 2], e, zp);
+          } else {
+            const uint32_t f = e - kHeadSlots;
+            put(conts[cb + (f / kChunkSlots) * wpc + h * 4 + (f % kChunkSlots) / 2], f, zp);
+          }
+        }
       }
+      steps += it.len;
     }
-    s.warp_steps[w] = static_cast<uint32_t>(st.size() / 4);
-    s.steps_max = std::max(s.steps_max, s.warp_steps[w]);
-    s.steps_total += s.warp_steps[w];
+    s.steps_max = std::max(s.steps_max, steps);
+    s.steps_total += steps;
   }
-  if (s.steps_max > kMaxWarpSteps) return;  // too much work per tile for the register schedule
-  s.regs = s.steps_max <= 16u * kStepsPerReg ? 16 : kSchedRegsMax;
-  // word layout per warp: word (r*32 + lane) = register r of lane `lane`; step e, group q is
-  // the (q&1) half of stream word 2e + (q>>1) -> register (2e+(q>>1))/32, lane (2e+(q>>1))%32
-  const uint32_t wpw = s.regs * 32;
-  s.words.assign(static_cast<size_t>(kConsumerWarps) * wpw, (static_cast<uint32_t>(kIdle) << 16) | kIdle);
-  for (int w = 0; w < kConsumerWarps; ++w) {
-    const std::vector<uint16_t> &st = streams[w];
-    for (size_t e = 0; e < st.size() / 4; ++e)
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t word = static_cast<uint32_t>(2 * e + (q >> 1));
-        uint32_t &dst = s.words[static_cast<size_t>(w) * wpw + word];
-        const uint32_t v = st[e * 4 + q];
-        dst = (q & 1) ? ((dst & 0x0000FFFFu) | (v << 16)) : ((dst & 0xFFFF0000u) | v);
-      }
-  }
+  heads.resize(heads.size() + kStreamPad * wpc, 0);
+  conts.resize(conts.size() + kStreamPad * wpc, 0);
+  s.cont_base = static_cast<uint32_t>(heads.size() / wpc);
+  s.words = std::move(heads);
+  s.words.insert(s.words.end(), conts.begin(), conts.end());
   g.smem_eligible = true;
 }
 

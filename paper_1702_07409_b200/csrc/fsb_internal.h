@@ -9,55 +9,67 @@
 namespace fsb {
 
 // ----------------------------------------------------------------- SMEM kernel geometry
-// A tile = (stripe, 128-byte slice of every symbol).  Its K intermediate rows are staged
-// in shared memory in units of kUnitRows rows (one TMA box of kUnitRows x 128 B each).
-constexpr int kSliceBytes = 128;
-constexpr int kUnitRows = 32;
+// A tile = (stripe, 64-byte slice of every symbol): its K intermediate rows, 64 B each, staged
+// in shared memory in units of kUnitRows rows (one TMA box of kUnitRows x 64 B).  Two tile
+// buffers (double buffering) plus the per-tile LT schedule fit in shared memory.
+constexpr int kSliceBytes = 64;
+constexpr int kUnitRows = 64;
 constexpr int kUnitBytes = kUnitRows * kSliceBytes;     // 4 KiB
 constexpr int kConsumerWarps = 16;
-constexpr int kGroupsPerWarp = 4;                        // 8 lanes x 16 B = one 128-B row
-constexpr int kGroups = kConsumerWarps * kGroupsPerWarp;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;      // + 1 TMA producer warp
+constexpr int kHalvesPerWarp = 8;                        // half-groups: 4 lanes x 16 B = 64 B
+constexpr int kThreads = (kConsumerWarps + 1) * 32;      // + 1 producer warp (TMA + precode)
 constexpr int kSplitThreshold = 32;                      // rows of degree > this are split
-                                                         // over the 4 groups of a warp
-// Register-resident schedule: each warp keeps its whole per-tile step stream in registers
-// (kSchedRegsMax 32-bit words per lane = 16 steps per word) and fetches step e of its lane
-// group with one warp shuffle.
-constexpr int kStepsPerReg = 16;
-constexpr int kSchedRegsMax = 32;
-constexpr uint32_t kMaxWarpSteps = kStepsPerReg * kSchedRegsMax;
-// 16-bit step values (one per lane group and step):
-constexpr uint16_t kIdle = 0x7FFF;        // no edge this step (row shorter than the item)
-constexpr uint16_t kStoreFlag = 0x8000;   // store step: 0x8000 | row  (row < 0x4000)
-constexpr uint16_t kSplitFlag = 0x4000;   //   split item: 0xC000 | row in all four groups
-constexpr uint16_t kStoreNone = 0xBFFF;   //   store step, nothing to store (row 0x3FFF; no split bit)
-constexpr uint32_t kMaxSmemRows = 0x3FFF; // n limit of the SMEM variant (rows 0..0x3FFE)
-constexpr uint32_t kMaxSmemSlots = 0x7FFE;
+                                                         // over the 8 half-groups of a warp
 
-// Host-built LT work schedule of the SMEM kernel (identical for every tile).
-// Rows of degree > kSplitThreshold are "split" items: their edges are dealt over the 4
-// lane groups of a warp and the partial XORs combined with two warp shuffles.  Other rows
-// are sorted by degree and packed 4 per item (one per 8-lane group) so the groups of a warp
-// run nearly equal edge counts in lockstep.  Items are dealt to warps longest-first onto
-// the least-loaded warp (LPT).  Each warp's stream is a sequence of steps; a step holds one
-// 16-bit value per group: a tile-relative source row (data m -> m, check i -> kpad+i), kIdle,
-// or (after an item's last edge) a store marker.  Stored as 32-bit words: step e, group g
-// is the (g&1) half of word 2e + (g>>1) of the warp's stream (see fsb_smem_encode).
+// Bank rule: a 128-bit shared load is served in phases of 8 lanes = two half-groups (lanes
+// 8q..8q+3 = half 0, 8q+4..8q+7 = half 1).  A 64-B row r occupies the 16 banks of half (r & 1)
+// of a 128-B line, so the two rows one phase reads are conflict-free iff their parities
+// differ.  The host schedule guarantees it: in every step, half 0 of group q reads an even row
+// exactly when half 1 reads an odd row (padding uses the even / odd zero rows).
+//
+// Item-record schedule.  A warp's per-tile LT work is a list of *items*; an item gives each of
+// the warp's 8 half-groups one output row and the same number L of source slots.  A slot is an
+// 11-bit tile row (data m -> m, check i -> kpad+i, padding -> zero_even / zero_odd); two slots
+// share a 32-bit word as  a | b << 21  (bits 11..20 zero), so the kernel forms the shared
+// address of `b` with one shift-add (sbase + (w >> 15)).  Two streams, copied into shared
+// memory once per CTA, in 128-byte chunks (8 half-groups x 16 B; half-group g's 16 B at uint4
+// index chunk*8 + g):
+//   heads: one chunk per item: word 0 = row | ctrl << 16, words 1..3 = slots 0..5; ctrl =
+//          L | split<<15 (identical in all 8 half-groups); row = kNoRow for an unused half;
+//   conts: slots 6.. of items with L > 6, 8 per chunk (4 words), items in the same order.
+// A split item spreads one heavy row over the 8 half-groups (evens to half 0, odds to half 1),
+// which then combine their partial XORs with three warp shuffles (same row in all 8).
+constexpr uint32_t kHeadSlots = 6;          // slots in an item's head chunk
+constexpr uint32_t kChunkSlots = 8;         // slots in a continuation chunk
+constexpr uint32_t kChunkBytes = kHalvesPerWarp * 16;
+constexpr uint32_t kStreamPad = 2;          // zero chunks after each stream (prefetch overrun)
+constexpr uint32_t kSlotBits = 11;
+constexpr uint32_t kSlotHiShift = 21;
+constexpr uint16_t kNoRow = 0xFFFF;
+constexpr uint16_t kSplitBit = 0x8000;
+constexpr uint32_t kMaxItemLen = 0x7FFF;
+constexpr uint32_t kMaxSmemRows = 0xFFFE;   // n limit of the SMEM variant (16-bit output rows)
+constexpr uint32_t kMaxSmemSlots = (1u << kSlotBits) - 1;  // tile rows (data + checks + zero rows)
+
+// Host-built LT work schedule of the SMEM kernel (identical for every tile; fsb_graph.cpp).
 struct SmemSchedule {
-  std::vector<uint32_t> words;          // kConsumerWarps x (regs*32) words
-  std::vector<uint32_t> warp_steps;     // steps per warp (incl. store steps)
-  std::vector<uint16_t> pre_slots;      // p * d_p tile-relative data rows
-  uint32_t regs = 0;                    // 32-bit schedule registers per lane (16 or 32)
+  std::vector<uint32_t> words;          // heads stream (+pad) then conts stream (+pad), uint32 words
+  uint32_t cont_base = 0;               // first chunk of the conts stream in `words`
+  std::vector<uint32_t> warp_info;      // kConsumerWarps x {items, head_off, cont_off} (chunks)
+  std::vector<uint16_t> pre_slots;      // p * d_p data rows
   uint32_t kpad = 0;                    // data rows rounded up to kUnitRows
-  uint32_t data_units = 0, check_units = 0, tile_units = 0;
-  uint32_t steps_max = 0, steps_total = 0;
+  uint32_t zero_even = 0;               // tile rows of the two all-zero padding rows
+  uint32_t tile_rows = 0;               // rows of a tile buffer (zero_even + 2)
+  uint32_t data_units = 0, tile_units = 0;
+  uint32_t steps_max = 0, steps_total = 0;  // gather slots per half-group per warp: max, sum
+  uint32_t pad_slots = 0;               // slots that read a zero row (parity / length padding)
 };
 
 struct DeviceBufs {
   int device = -1;
   int32_t *pre_row_ptr = nullptr, *pre_col = nullptr, *lt_row_ptr = nullptr, *lt_col = nullptr;
   uint32_t *sched = nullptr;
-  uint32_t *warp_steps = nullptr;
+  uint32_t *warp_info = nullptr;
   uint16_t *pre_slots = nullptr;
 };
 
@@ -74,7 +86,6 @@ struct Graph {
   int sm_count = 0;
   int smem_optin = 0;
   uint32_t smem_bytes = 0;   // dynamic smem of the SMEM kernel
-  uint32_t ring_units = 0;   // shared-memory units of the SMEM kernel
 };
 
 // fsb_graph.cpp

@@ -62,17 +62,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   } while (!done);
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int32_t c0,
-                                            int32_t c1, int32_t c2, uint64_t policy) {
+                                            int32_t c1, int32_t c2) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -92,169 +87,213 @@ __device__ __forceinline__ void st_stream(uint8_t *p, const uint4 &v) {
 
 // ============================================================================ SMEM kernel
 struct SmemArgs {
-  const uint32_t *sched;       // kConsumerWarps x (NR*32) schedule words
-  const uint32_t *warp_steps;  // kConsumerWarps
-  const uint16_t *pre_slots;   // p * d_p
+  const uint4 *sched;          // heads ++ conts chunk streams (fsb_internal.h: SmemSchedule)
+  const uint32_t *warp_info;   // kConsumerWarps x {items, head_off, cont_off}
+  const uint16_t *pre_slots;   // p * d_p data rows
   uint8_t *checks;
   uint64_t checks_stride;
   uint8_t *coded;
   uint64_t coded_stride;
   uint64_t t;
-  uint32_t nslices, ntiles, p, d_p, kpad, data_units, tile_units, ring_units;
+  uint32_t nslices, ntiles, p, d_p, kpad, zero_even, data_units, tile_units;
+  uint32_t sched_chunks, cont_base;
 };
 
-// Use index of ring unit x by the CTA's i-th tile (even tiles occupy [0,T), odd [U-T,U)).
-__device__ __forceinline__ uint32_t unit_use(uint32_t x, uint32_t i, uint32_t T, uint32_t U) {
-  const bool in_even = x < T, in_odd = x + T >= U;
-  return (in_even && in_odd) ? i : (i >> 1);
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4 &v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
 
-template <int NR>
-__device__ __forceinline__ void store_item(uint4 acc, uint32_t v, uint32_t grp, uint8_t *out, uint64_t t) {
-  if (v & kSplitFlag) {  // split row: combine the four groups' partial XORs (uniform branch)
+// Shared address of slot h (0..7) of chunk c: word h/2 holds slots a | b << 21 (fsb_internal.h);
+// tile row r lives at sbase + r*64.  h is a compile-time constant after unrolling.  Written in
+// PTX so ptxas sees the shift-adds (LEA / LEA.HI) instead of LLVM's canonical shl+and.
+__device__ __forceinline__ uint32_t slot_addr(const uint4 &c, int h, uint32_t sbase) {
+  const uint32_t w = (h >> 1) == 0 ? c.x : (h >> 1) == 1 ? c.y : (h >> 1) == 2 ? c.z : c.w;
+  uint32_t addr;
+  if (h & 1) {  // b = w >> 21, bits 11..20 zero: sbase + (w >> 15)
+    asm("{\n .reg .b32 t;\n shr.b32 t, %1, 15;\n add.u32 %0, t, %2;\n}" : "=r"(addr) : "r"(w), "r"(sbase));
+  } else {      // a = w & 0x7FF: sbase + (a << 6)
+    asm("{\n .reg .b32 t;\n and.b32 t, %1, 2047;\n mad.lo.u32 %0, t, 64, %2;\n}" : "=r"(addr) : "r"(w), "r"(sbase));
+  }
+  return addr;
+}
+
+// acc ^= tile rows named by slots [H0, H0+N) of chunk c.  All N shared-memory loads are issued
+// before the XOR chain so they overlap.
+template <int H0, int N>
+__device__ __forceinline__ void gather_xor(uint4 &acc, const uint4 &c, uint32_t sbase) {
+  uint4 x[N];
 #pragma unroll
-    for (int o = 8; o <= 16; o <<= 1) {
+  for (int i = 0; i < N; ++i) x[i] = lds128(slot_addr(c, H0 + i, sbase));
+#pragma unroll
+  for (int i = 0; i < N; ++i) xor_into(acc, x[i]);
+}
+
+template <int H0>
+__device__ __forceinline__ void gather_xor_n(uint4 &acc, const uint4 &c, uint32_t n, uint32_t sbase) {
+  switch (n) {
+    case 1: gather_xor<H0, 1>(acc, c, sbase); break;
+    case 2: gather_xor<H0, 2>(acc, c, sbase); break;
+    case 3: gather_xor<H0, 3>(acc, c, sbase); break;
+    case 4: gather_xor<H0, 4>(acc, c, sbase); break;
+    case 5: if (H0 + 5 <= 8) gather_xor<H0, (H0 + 5 <= 8 ? 5 : 1)>(acc, c, sbase); break;
+    case 6: if (H0 + 6 <= 8) gather_xor<H0, (H0 + 6 <= 8 ? 6 : 1)>(acc, c, sbase); break;
+    case 7: if (H0 + 7 <= 8) gather_xor<H0, (H0 + 7 <= 8 ? 7 : 1)>(acc, c, sbase); break;
+    default: if (H0 == 0) gather_xor<H0, (H0 == 0 ? 8 : 1)>(acc, c, sbase); break;
+  }
+}
+
+// One item (fsb_internal.h): head chunk h, continuation chunks at *cp (shared address, advanced),
+// XOR in registers, one 64-B store per half-group (split items: combined over the 8 halves).
+__device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t sbase, uint8_t *out, uint64_t t,
+                                        uint32_t half_id) {
+  const uint32_t row = h.x & 0xFFFFu;
+  const uint32_t ctrl = h.x >> 16;
+  const uint32_t L = ctrl & kMaxItemLen;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  gather_xor_n<2>(acc, h, L < kHeadSlots ? L : kHeadSlots, sbase);
+  if (L > kHeadSlots) {
+    uint32_t rem = L - kHeadSlots;
+    uint4 c = lds128(cp);
+    cp += kChunkBytes;
+    for (; rem > kChunkSlots; rem -= kChunkSlots) {
+      const uint4 nx = lds128(cp);  // next chunk in flight while this one is gathered
+      cp += kChunkBytes;
+      gather_xor<0, 8>(acc, c, sbase);
+      c = nx;
+    }
+    gather_xor_n<0>(acc, c, rem, sbase);
+  }
+  if (ctrl & kSplitBit) {  // split row: combine the eight half-groups' partial XORs
+#pragma unroll
+    for (int o = 4; o <= 16; o <<= 1) {
       acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, o);
       acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, o);
       acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, o);
       acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, o);
     }
-    if (grp == 0) st_stream(out + static_cast<uint64_t>(v & 0x3FFF) * t, acc);
-  } else if ((v & 0x3FFF) != 0x3FFF) {
-    st_stream(out + static_cast<uint64_t>(v & 0x3FFF) * t, acc);
+    if (half_id == 0) st_stream(out + static_cast<uint64_t>(row) * t, acc);
+  } else if (row != kNoRow) {
+    st_stream(out + static_cast<uint64_t>(row) * t, acc);
   }
 }
 
-template <int NR>
+// Persistent encode kernel, one CTA per SM.  Shared memory: two tile buffers (tile_units x 4 KiB
+// each), the LT schedule, then the mbarriers.  Warp roles:
+//   producer warp (16): lane 0 streams each tile's data rows in by TMA (box kUnitRows x 64 B);
+//     then the whole warp computes the tile's p precode checks (PAPER.md:91 step (1)) from
+//     shared memory into the buffer's check rows and to HBM, and signals `ready`;
+//   consumer warps (0..15): every LT row (PAPER.md:91 step (2)) of the tile as a register XOR of
+//     64-B rows gathered from shared memory, one 64-B store per row.
+// Buffers alternate (tile i uses buffer i&1), so tile i+1 streams in while tile i computes, and a
+// consumer warp that finishes tile i early starts tile i+1 without waiting for the others.
 __global__ void __launch_bounds__(kThreads, 1)
     fsb_smem_encode(const __grid_constant__ CUtensorMap tmap, const SmemArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const uint32_t U = a.ring_units, T = a.tile_units;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + static_cast<size_t>(U) * kUnitBytes);
-  uint64_t *empty = full + U;
+  const uint32_t T = a.tile_units;
+  const uint32_t buf_bytes = T * kUnitBytes;
+  uint8_t *sched_s = smem + 2 * static_cast<size_t>(buf_bytes);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sched_s + static_cast<size_t>(a.sched_chunks) * kChunkBytes);
+  uint64_t *full = bars, *ready = bars + 2, *empty = bars + 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t smem_base = smem_u32(smem);
 
   if (threadIdx.x == 0) {
-    for (uint32_t x = 0; x < U; ++x) {
-      mbar_init(smem_u32(&full[x]), 1);
-      mbar_init(smem_u32(&empty[x]), kConsumerWarps);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&full[b]), 1);
+      mbar_init(smem_u32(&ready[b]), 1);
+      mbar_init(smem_u32(&empty[b]), kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // the schedule (identical for every tile) and the two zero rows of each buffer
+  for (uint32_t x = threadIdx.x; x < a.sched_chunks * (kChunkBytes / 16); x += blockDim.x)
+    sts128(smem_u32(sched_s) + x * 16, __ldg(a.sched + x));
+  if (threadIdx.x < 2 * 2 * (kSliceBytes / 16)) {  // 2 buffers x 2 rows x 4 lanes
+    const uint32_t b = threadIdx.x >> 3, r = (threadIdx.x >> 2) & 1, l4 = threadIdx.x & 3;
+    sts128(smem_base + b * buf_bytes + (a.zero_even + r) * kSliceBytes + l4 * 16, make_uint4(0, 0, 0, 0));
+  }
   __syncthreads();
 
-  const uint32_t ov = (2 * T > U) ? 2 * T - U : 0;  // units shared by consecutive tiles
-
   if (warp == kConsumerWarps) {
-    // ------------------------------------------------------------ TMA producer (1 lane)
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-      const uint64_t pol = policy_evict_first();
-      uint32_t i = 0;
-      for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
-        const uint32_t stripe = tile / a.nslices, slice = tile % a.nslices;
-        const uint32_t base = (i & 1) ? U - T : 0;
-        for (uint32_t j = 0; j < T; ++j) {
-          // units private to this parity first, the units shared with the previous tile last
-          const uint32_t u = (i & 1) ? (j + ov) % T : j;
-          const uint32_t x = base + u;
-          const uint32_t use = unit_use(x, i, T, U);
-          mbar_wait(smem_u32(&empty[x]), (use & 1) ^ 1);
-          if (u < a.data_units) {
-            mbar_arrive_expect_tx(smem_u32(&full[x]), kUnitBytes);
-            tma_load_3d(smem_u32(smem + static_cast<size_t>(x) * kUnitBytes), &tmap, smem_u32(&full[x]),
-                        static_cast<int32_t>(slice * kSliceBytes), static_cast<int32_t>(u * kUnitRows),
-                        static_cast<int32_t>(stripe), pol);
-          } else {
-            mbar_arrive(smem_u32(&full[x]));  // check rows: written by the consumers
-          }
-        }
+    // ------------------------------------------------------- producer: TMA + precode checks
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    const uint32_t half_id = lane >> 2, lane4 = lane & 3;
+    uint32_t i = 0;
+    for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
+      const uint32_t b = i & 1, ph = (i >> 1) & 1;
+      const uint32_t stripe = tile / a.nslices, slice = tile % a.nslices;
+      const uint32_t buf = smem_base + b * buf_bytes;
+      if (lane == 0) {
+        mbar_wait(smem_u32(&empty[b]), ph ^ 1);  // consumers released tile i-2
+        mbar_arrive_expect_tx(smem_u32(&full[b]), a.data_units * kUnitBytes);
+        for (uint32_t u = 0; u < a.data_units; ++u)
+          tma_load_3d(buf + u * kUnitBytes, &tmap, smem_u32(&full[b]), static_cast<int32_t>(slice * kSliceBytes),
+                      static_cast<int32_t>(u * kUnitRows), static_cast<int32_t>(stripe));
       }
+      __syncwarp();
+      mbar_wait(smem_u32(&full[b]), ph);
+      // precode: check c by half-group c % 8, 16 B per lane
+      const uint32_t lb = buf + lane4 * 16;
+      const uint64_t col_off = static_cast<uint64_t>(slice) * kSliceBytes + lane4 * 16;
+      for (uint32_t c = half_id; c < a.p; c += kHalvesPerWarp) {
+        uint4 acc = make_uint4(0, 0, 0, 0);
+        for (uint32_t e = 0; e < a.d_p; ++e) {
+          const uint32_t r = __ldg(&a.pre_slots[c * a.d_p + e]);
+          xor_into(acc, lds128(lb + r * kSliceBytes));
+        }
+        sts128(lb + (a.kpad + c) * kSliceBytes, acc);
+        st_stream(a.checks + stripe * a.checks_stride + c * a.t + col_off, acc);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&ready[b]));  // release: data + checks visible
     }
     return;
   }
 
   // ------------------------------------------------------------------- consumer warps
-  const uint4 *ring4 = reinterpret_cast<const uint4 *>(smem);
-  uint4 *ring4w = reinterpret_cast<uint4 *>(smem);
-  const uint32_t grp = lane >> 3, lane8 = lane & 7;
-  const uint32_t gidx = warp * kGroupsPerWarp + grp;
-  // this warp's whole LT schedule lives in registers for the kernel's lifetime
-  uint32_t R[NR];
-  {
-    const uint32_t *sw = a.sched + static_cast<size_t>(warp) * (NR * 32);
-#pragma unroll
-    for (int r = 0; r < NR; ++r) R[r] = __ldg(&sw[r * 32 + lane]);
-  }
-  const uint32_t nsteps = __ldg(&a.warp_steps[warp]);
-  const uint32_t src_hi = grp >> 1, sh = (grp & 1) * 16;
+  const uint32_t half_id = lane >> 2, lane4 = lane & 3;
+  const uint32_t nitems = __ldg(&a.warp_info[warp * 3 + 0]);
+  const uint32_t head0 = smem_u32(sched_s) + __ldg(&a.warp_info[warp * 3 + 1]) * kChunkBytes + half_id * 16;
+  const uint32_t cont0 =
+      smem_u32(sched_s) + (a.cont_base + __ldg(&a.warp_info[warp * 3 + 2])) * kChunkBytes + half_id * 16;
   uint32_t i = 0;
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
+    const uint32_t b = i & 1, ph = (i >> 1) & 1;
     const uint32_t stripe = tile / a.nslices, slice = tile % a.nslices;
-    const uint32_t base_unit = (i & 1) ? U - T : 0;
-    const uint32_t tbase = base_unit * (kUnitBytes / 16) + lane8;  // uint4 index of row 0, my lane
-    for (uint32_t u = 0; u < T; ++u) {
-      const uint32_t x = base_unit + u;
-      mbar_wait(smem_u32(&full[x]), unit_use(x, i, T, U) & 1);
+    const uint32_t sbase = smem_base + b * buf_bytes + lane4 * 16;  // this lane's 16 B of tile row 0
+    uint32_t hp = head0, cp = cont0;
+    uint4 h0 = lds128(hp);
+    mbar_wait(smem_u32(&ready[b]), ph);
+    mbar_wait(smem_u32(&full[b]), ph);
+    uint8_t *out = a.coded + stripe * a.coded_stride + static_cast<uint64_t>(slice) * kSliceBytes + lane4 * 16;
+    // items, with the next head chunk in flight (2-way unrolled so no register moves)
+    for (uint32_t it = 0; it < nitems; it += 2) {
+      const uint4 h1 = lds128(hp + kChunkBytes);
+      lt_item(h0, cp, sbase, out, a.t, half_id);
+      if (it + 1 >= nitems) break;
+      h0 = lds128(hp + 2 * kChunkBytes);
+      hp += 2 * kChunkBytes;
+      lt_item(h1, cp, sbase, out, a.t, half_id);
     }
-    const uint64_t col_off = static_cast<uint64_t>(slice) * kSliceBytes + lane8 * 16;
-
-    // (1) precode checks (PAPER.md:91 step (1)): into the tile's check rows and to HBM
-    if (a.p) {
-      for (uint32_t c = gidx; c < a.p; c += kGroups) {
-        uint4 acc = make_uint4(0, 0, 0, 0);
-        for (uint32_t e = 0; e < a.d_p; ++e) {
-          const uint32_t s = __ldg(&a.pre_slots[c * a.d_p + e]);
-          xor_into(acc, ring4[tbase + s * 8]);
-        }
-        ring4w[tbase + (a.kpad + c) * 8] = acc;
-        st_stream(a.checks + stripe * a.checks_stride + c * a.t + col_off, acc);
-      }
-      consumer_bar();
-    }
-
-    // (2) LT rows (PAPER.md:91 step (2)): step e of group grp is a warp shuffle away
-    uint8_t *out = a.coded + stripe * a.coded_stride + col_off;
-    uint4 acc = make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      if (static_cast<uint32_t>(r) * kStepsPerReg >= nsteps) break;
-      const uint32_t reg = R[r];
-      for (uint32_t q = 0; q < static_cast<uint32_t>(kStepsPerReg); q += 4) {
-        if (r * kStepsPerReg + q >= nsteps) break;
-        uint32_t v[4];
-        uint4 x[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = (__shfl_sync(0xffffffffu, reg, 2 * (q + j) + src_hi) >> sh) & 0xFFFF;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          x[j] = make_uint4(0, 0, 0, 0);
-          if (v[j] < kIdle) x[j] = ring4[tbase + v[j] * 8];
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (v[j] & kStoreFlag) {  // store step: the same for every group of the warp
-            store_item<NR>(acc, v[j], grp, out, a.t);
-            acc = make_uint4(0, 0, 0, 0);
-          } else {
-            xor_into(acc, x[j]);
-          }
-        }
-      }
-    }
-    // release the tile's units to the producer
-    fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) {
-      for (uint32_t u = 0; u < T; ++u) mbar_arrive(smem_u32(&empty[base_unit + u]));
-    }
+    if (lane == 0) mbar_arrive(smem_u32(&empty[b]));
   }
 }
 
 // ========================================================================= GLOBAL kernels
 constexpr int kGlobalThreads = 256;
 constexpr int kGroupsPerBlock = kGlobalThreads / 8;
-constexpr uint32_t kBandSlices = 4;  // 512-B bands: one warp = one row x 4 slices
+constexpr uint32_t kGSliceBytes = 128;  // one 8-lane group = 8 x 16 B
+constexpr uint32_t kBandSlices = 4;    // 512-B bands: one warp = one row x 4 slices
 
 __global__ void __launch_bounds__(kGlobalThreads)
     fsb_precode_global(uint32_t S, uint32_t p, uint32_t d_p, uint64_t t, uint32_t nslices,
@@ -268,7 +307,7 @@ __global__ void __launch_bounds__(kGlobalThreads)
   const uint64_t r = item / nslices;
   const uint32_t c = r % p;
   const uint32_t s = static_cast<uint32_t>(r / p);
-  const uint64_t byte = static_cast<uint64_t>(slice) * kSliceBytes + lane8 * 16;
+  const uint64_t byte = static_cast<uint64_t>(slice) * kGSliceBytes + lane8 * 16;
   if (byte >= t) return;
   const uint8_t *src = data + s * data_stride + byte;
   uint4 acc = make_uint4(0, 0, 0, 0);
@@ -295,7 +334,7 @@ __global__ void __launch_bounds__(kGlobalThreads)
   const uint64_t s = e / nbands;
   if (s >= S) return;
   const uint32_t slice = band * kBandSlices + q;
-  const uint64_t byte = static_cast<uint64_t>(slice) * kSliceBytes + lane8 * 16;
+  const uint64_t byte = static_cast<uint64_t>(slice) * kGSliceBytes + lane8 * 16;
   if (slice >= nslices || byte >= t) return;
   const uint32_t j = row_begin + jr;
   const uint8_t *dsrc = data + s * data_stride + byte;
@@ -369,7 +408,7 @@ void free_device(Graph &g) {
   cudaFree(d.lt_row_ptr);
   cudaFree(d.lt_col);
   cudaFree(d.sched);
-  cudaFree(d.warp_steps);
+  cudaFree(d.warp_info);
   cudaFree(d.pre_slots);
   if (prev >= 0) cudaSetDevice(prev);
   d = DeviceBufs();
@@ -390,22 +429,17 @@ fs_status upload_graph(Graph &g) {
   if ((st = upload(&g.dev.lt_row_ptr, g.lt_row_ptr.data(), g.lt_row_ptr.size())) != FS_OK) return st;
   if ((st = upload(&g.dev.lt_col, g.lt_col.data(), g.lt_col.size())) != FS_OK) return st;
   if (g.smem_eligible) {
-    // ring size: as many 4-KiB units as the opt-in shared memory allows (barriers after them)
-    uint32_t units = static_cast<uint32_t>((g.smem_optin - 1024) / (kUnitBytes + 16));
-    if (const char *env = std::getenv("FSB_RING_UNITS")) units = std::min<uint32_t>(units, std::atoi(env));
-    g.ring_units = units;
-    g.smem_bytes = units * kUnitBytes + units * 16;
-    if (g.sched.tile_units > units || g.sched.tile_units == 0) {
+    // two tile buffers + the schedule + 6 mbarriers
+    const uint64_t bytes = 2ull * g.sched.tile_units * kUnitBytes + g.sched.words.size() * 4 + 6 * 8;
+    g.smem_bytes = static_cast<uint32_t>(bytes);
+    if (bytes > static_cast<uint64_t>(g.smem_optin)) {
       g.smem_eligible = false;
     } else {
       if ((st = upload(&g.dev.sched, g.sched.words.data(), g.sched.words.size())) != FS_OK) return st;
-      if ((st = upload(&g.dev.warp_steps, g.sched.warp_steps.data(), g.sched.warp_steps.size())) != FS_OK) return st;
+      if ((st = upload(&g.dev.warp_info, g.sched.warp_info.data(), g.sched.warp_info.size())) != FS_OK) return st;
       if ((st = upload(&g.dev.pre_slots, g.sched.pre_slots.data(), g.sched.pre_slots.size())) != FS_OK) return st;
-      e = cudaFuncSetAttribute(fsb_smem_encode<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(fsb_smem_encode, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(g.smem_bytes));
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(fsb_smem_encode<kSchedRegsMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(g.smem_bytes));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     }
   }
@@ -448,8 +482,8 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
       return FS_ECUDA;
     }
     SmemArgs a;
-    a.sched = g.dev.sched;
-    a.warp_steps = g.dev.warp_steps;
+    a.sched = reinterpret_cast<const uint4 *>(g.dev.sched);
+    a.warp_info = g.dev.warp_info;
     a.pre_slots = g.dev.pre_slots;
     a.checks = checks;
     a.checks_stride = checks_stride;
@@ -461,34 +495,34 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     a.p = prm.p;
     a.d_p = prm.d_p;
     a.kpad = g.sched.kpad;
+    a.zero_even = g.sched.zero_even;
     a.data_units = g.sched.data_units;
     a.tile_units = g.sched.tile_units;
-    a.ring_units = g.ring_units;
+    a.sched_chunks = static_cast<uint32_t>(g.sched.words.size() / (kChunkBytes / 4));
+    a.cont_base = g.sched.cont_base;
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, g.sm_count));
-    if (g.sched.regs <= 16)
-      fsb_smem_encode<16><<<grid, kThreads, g.smem_bytes, stream>>>(tmap, a);
-    else
-      fsb_smem_encode<kSchedRegsMax><<<grid, kThreads, g.smem_bytes, stream>>>(tmap, a);
+    fsb_smem_encode<<<grid, kThreads, g.smem_bytes, stream>>>(tmap, a);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_smem_encode launch");
     *launches = 1;
     return FS_OK;
   }
+  const uint32_t gslices = static_cast<uint32_t>((prm.t + kGSliceBytes - 1) / kGSliceBytes);
   if (prm.p) {
-    const uint64_t items = static_cast<uint64_t>(S) * prm.p * nslices;
+    const uint64_t items = static_cast<uint64_t>(S) * prm.p * gslices;
     const uint64_t blocks = (items + kGroupsPerBlock - 1) / kGroupsPerBlock;
     fsb_precode_global<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, prm.p, prm.d_p, prm.t, nslices, g.dev.pre_col, data, data_stride, checks, checks_stride);
+        S, prm.p, prm.d_p, prm.t, gslices, g.dev.pre_col, data, data_stride, checks, checks_stride);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_precode_global launch");
     ++*launches;
   }
   const uint32_t nrows = row_end - row_begin;
   if (nrows) {
-    const uint32_t nbands = (nslices + kBandSlices - 1) / kBandSlices;
+    const uint32_t nbands = (gslices + kBandSlices - 1) / kBandSlices;
     const uint64_t items = static_cast<uint64_t>(S) * nbands * nrows * kBandSlices;
     const uint64_t blocks = (items + kGroupsPerBlock - 1) / kGroupsPerBlock;
     if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
     fsb_lt_global<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, prm.k, prm.t, nslices, nbands, row_begin, nrows, g.dev.lt_row_ptr, g.dev.lt_col, data, data_stride,
+        S, prm.k, prm.t, gslices, nbands, row_begin, nrows, g.dev.lt_row_ptr, g.dev.lt_col, data, data_stride,
         checks, checks_stride, coded, coded_stride);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_lt_global launch");
     ++*launches;

@@ -145,48 +145,71 @@ def test_schedule_balance():
         g = fsb.Graph.create(configs.get(cid), host_only=True)
         inf = g.info()
         assert inf["smem_eligible"] == 1
-        assert inf["sched_steps_avg"] * 16 >= inf["lt_nnz"] // 4
-        assert inf["sched_steps_max"] <= 1.05 * inf["sched_steps_avg"] + 4
+        # steps are per half-group (8 per warp, 16 warps); padding (parity + length) below 15%
+        assert inf["sched_steps_avg"] * 16 * 8 >= inf["lt_nnz"]
+        assert inf["sched_steps_avg"] * 16 * 8 <= 1.15 * inf["lt_nnz"] + 16 * 8
+        assert inf["sched_steps_max"] <= 1.08 * inf["sched_steps_avg"] + 8
 
 
 def _simulate_schedule(g, c):
-    """Replays the SMEM kernel's consumption of its register schedule (fsb_smem_encode) on
-    the host: returns {row: sorted tile-relative slots} and asserts store steps are
-    warp-uniform (the kernel's shuffles rely on it)."""
-    words, steps, kpad = g.schedule()
+    """Replays the SMEM kernel's consumption of its two chunk streams (fsb_smem_encode) on the
+    host: returns {row: sorted tile rows}.  Asserts that every item's control half is identical
+    in the 8 half-groups (the kernel's dispatch and split shuffles rely on it) and the bank rule:
+    in every step, half 0 of a group reads an even tile row iff half 1 reads an odd one."""
+    words, cont_base, info, kpad, z0 = g.schedule()
+    words = words.astype(np.int64)
+    lo, hi = words & 0x7FF, words >> 21
+    slots = np.stack([lo, hi], axis=1).reshape(-1, 8, 8)   # [chunk, half-group, slot position]
+    chunks = words.reshape(-1, 8, 4)                       # [chunk, half-group, word]
+    heads, conts = chunks[:cont_base], slots[cont_base:]
+    head_slots = slots[:cont_base]
+    assert np.all((words[cont_base * 32:] >> 11) & 0x3FF == 0)
     rows = {}
+    hpos, cpos = 0, 0
+    zeros = (z0, z0 + 1)
     for w in range(16):
-        flat = words[w].reshape(-1)            # word index = r*32 + lane
-        acc = [[] for _ in range(4)]
-        for e in range(int(steps[w])):
-            vals = []
-            for q in range(4):
-                word = int(flat[2 * e + (q >> 1)])
-                vals.append((word >> (16 * (q & 1))) & 0xFFFF)
-            stores = [v >= 0x8000 for v in vals]
-            assert all(stores) or not any(stores), "non-uniform store step"
-            if all(stores):
-                splits = [bool(v & 0x4000) for v in vals]
-                assert all(splits) or not any(splits), "non-uniform split flag"
-                if all(splits):
-                    assert len(set(vals)) == 1
-                    row = vals[0] & 0x3FFF
-                    assert row not in rows
-                    rows[row] = sorted(sum(acc, []))
-                else:
-                    for q in range(4):
-                        row = vals[q] & 0x3FFF
-                        if row != 0x3FFF:
-                            assert row not in rows
-                            rows[row] = sorted(acc[q])
-                acc = [[] for _ in range(4)]
-            else:
+        nitems, hoff, coff = (int(x) for x in info[w])
+        assert (hoff, coff) == (hpos, cpos)
+        for _ in range(nitems):
+            head = heads[hpos]
+            hslots = head_slots[hpos]
+            hpos += 1
+            assert all(((int(head[h, j]) >> 11) & 0x3FF) == 0 for h in range(8) for j in (1, 2, 3))
+            ctrls = set(int(head[h, 0]) >> 16 for h in range(8))
+            assert len(ctrls) == 1, "non-uniform item control"
+            ctrl = ctrls.pop()
+            L, split = ctrl & 0x7FFF, bool(ctrl & 0x8000)
+            assert L >= 1
+            per = [[] for _ in range(8)]
+            for e in range(L):
+                vals = []
+                for h in range(8):
+                    if e < 6:
+                        v = int(hslots[h, 2 + e])
+                    else:
+                        f = e - 6
+                        v = int(conts[cpos + f // 8, h, f % 8])
+                    vals.append(v)
+                    if v not in zeros:
+                        per[h].append(v)
                 for q in range(4):
-                    if vals[q] < 0x7FFF:
-                        acc[q].append(vals[q])
-        assert not any(acc), "edges after the last store step"
-        rest = flat[2 * int(steps[w]):]
-        assert np.all(rest == 0x7FFF7FFF)
+                    assert (vals[2 * q] & 1) != (vals[2 * q + 1] & 1), "bank rule"
+            cpos += 0 if L <= 6 else (L - 6 + 7) // 8
+            outs = [int(head[h, 0]) & 0xFFFF for h in range(8)]
+            if split:
+                assert len(set(outs)) == 1 and outs[0] != 0xFFFF
+                assert outs[0] not in rows
+                rows[outs[0]] = sorted(sum(per, []))
+            else:
+                for h in range(8):
+                    if outs[h] == 0xFFFF:
+                        assert not per[h]
+                        continue
+                    assert outs[h] not in rows
+                    rows[outs[h]] = sorted(per[h])
+    # prefetch padding after each stream
+    assert len(heads) - hpos == 2 and np.all(heads[hpos:] == 0)
+    assert len(conts) - cpos == 2 and np.all(conts[cpos:] == 0)
     return rows, kpad
 
 
