@@ -156,15 +156,15 @@ FSB_API fs_status fs_encode_stripes(const fs_graph *g, uint32_t num_stripes,
  * words[nwords] = two chunk streams of uint32 words, the heads stream first and the conts stream
  * from chunk cont_base on (chunk c = words 32c..32c+31; half-group h's 4 words at 32c+4h; half-
  * group h = lanes 4h..4h+3 of a warp, h = 2*group + half).  warp_info[16*3] = {items, first head
- * chunk, first cont chunk} per consumer warp.  A slot is an 11-bit tile row (data m -> m, check i
+ * chunk, first cont chunk} per consumer warp (nwarps of them).  A slot is an 11-bit tile row (data m -> m, check i
  * -> kpad+i, padding -> zero_even or zero_even+1); a slot word packs two slots as a | b << 21.
  * An item's head chunk holds, per half-group, word 0 = row | ctrl << 16 (ctrl = L | split << 15;
  * row 0xFFFF = no output) and slots 0..5 in words 1..3; slots 6..L-1 follow in the conts stream,
  * 8 per chunk.  In every step, half 0 of a group reads an even row iff half 1 reads an odd one
  * (shared-memory bank rule).  FS_EUNSUPPORTED when the graph is not SMEM-eligible.          */
 FSB_API fs_status fs_graph_schedule(const fs_graph *g, const uint32_t **words, uint64_t *nwords,
-                                    uint32_t *cont_base, const uint32_t **warp_info, uint32_t *kpad,
-                                    uint32_t *zero_even);
+                                    uint32_t *cont_base, const uint32_t **warp_info, uint32_t *nwarps,
+                                    uint32_t *kpad, uint32_t *zero_even);
 
 /* Number of kernel launches the last successful fs_encode / fs_encode_stripes on this
  * thread enqueued (for launch accounting in benchmarks).                                 */

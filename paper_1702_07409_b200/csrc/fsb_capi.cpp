@@ -218,7 +218,7 @@ fs_status fs_encode_stripes(const fs_graph *h, uint32_t S, const uint8_t *d_data
 }
 
 fs_status fs_graph_schedule(const fs_graph *h, const uint32_t **words, uint64_t *nwords, uint32_t *cont_base,
-                            const uint32_t **warp_info, uint32_t *kpad, uint32_t *zero_even) {
+                            const uint32_t **warp_info, uint32_t *nwarps, uint32_t *kpad, uint32_t *zero_even) {
   if (!h) { set_error("null graph"); return FS_EINVAL; }
   const fsb::Graph &g = h->g;
   if (!g.smem_eligible || g.sched.words.empty()) { set_error("graph has no SMEM schedule"); return FS_EUNSUPPORTED; }
@@ -226,6 +226,7 @@ fs_status fs_graph_schedule(const fs_graph *h, const uint32_t **words, uint64_t 
   if (nwords) *nwords = g.sched.words.size();
   if (cont_base) *cont_base = g.sched.cont_base;
   if (warp_info) *warp_info = g.sched.warp_info.data();
+  if (nwarps) *nwarps = fsb::kConsumerWarps;
   if (kpad) *kpad = g.sched.kpad;
   if (zero_even) *zero_even = g.sched.zero_even;
   return FS_OK;

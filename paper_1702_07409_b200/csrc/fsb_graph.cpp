@@ -12,6 +12,8 @@
 #include <cstring>
 #include <numeric>
 #include <queue>
+#include <cstdlib>
+#include <string>
 
 #include "fsb_internal.h"
 
@@ -349,6 +351,14 @@ void build_smem_schedule(Graph &g) {
     heap.pop();
     per_warp[l.second].push_back(idx);
     heap.push({l.first + cost(items[idx]), l.second});
+  }
+  // profiling experiment (FSB_SCHED_DEBUG=zero): every slot reads a zero row of its half's parity
+  if (const char *dbg = std::getenv("FSB_SCHED_DEBUG")) {
+    if (std::string(dbg) == "zero")
+      for (Item &it : items)
+        for (int q = 0; q < 4; ++q)
+          for (int hh = 0; hh < 2; ++hh)
+            for (uint16_t &v : it.grp[q].seq[hh]) v = hh ? z1 : z0;
   }
   // emit the two chunk streams, warp after warp (32 words per chunk; half-group h: words 4h..4h+3)
   s.warp_info.assign(kConsumerWarps * 3, 0);

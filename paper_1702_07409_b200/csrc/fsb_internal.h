@@ -15,7 +15,7 @@ namespace fsb {
 constexpr int kSliceBytes = 64;
 constexpr int kUnitRows = 64;
 constexpr int kUnitBytes = kUnitRows * kSliceBytes;     // 4 KiB
-constexpr int kConsumerWarps = 16;
+constexpr int kConsumerWarps = 20;
 constexpr int kHalvesPerWarp = 8;                        // half-groups: 4 lanes x 16 B = 64 B
 constexpr int kThreads = (kConsumerWarps + 1) * 32;      // + 1 producer warp (TMA + precode)
 constexpr int kSplitThreshold = 32;                      // rows of degree > this are split

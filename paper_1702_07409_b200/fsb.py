@@ -68,7 +68,7 @@ def lib():
         L.fs_encode.argtypes = [P, P, P, P, u32, u32, P]
         L.fs_encode_stripes.argtypes = [P, u32, P, u64, P, u64, P, u64, P]
         L.fs_graph_schedule.argtypes = [P, PP, ctypes.POINTER(u64), ctypes.POINTER(u32), PP,
-                                        ctypes.POINTER(u32), ctypes.POINTER(u32)]
+                                        ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u32)]
         for f in ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get_info",
                   "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_graph_schedule"):
             getattr(L, f).restype = ctypes.c_int
@@ -179,16 +179,18 @@ class Graph:
         return {f: getattr(inf, f) for f, _ in fs_graph_info._fields_}
 
     def schedule(self):
-        """(words uint32[nwords], cont_base, warp_info uint32[16,3], kpad, zero_row) of the SMEM
-        schedule (copies; format in include/fsb.h)."""
+        """(words uint32[nwords], cont_base, warp_info uint32[nwarps,3], kpad, zero_even) of the
+        SMEM schedule (copies; format in include/fsb.h)."""
         w, wi = ctypes.c_void_p(), ctypes.c_void_p()
         nw = ctypes.c_uint64()
-        cb, kpad, zr = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        cb, nwarps, kpad, z0 = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
         _check(lib().fs_graph_schedule(self._h, ctypes.byref(w), ctypes.byref(nw), ctypes.byref(cb),
-                                       ctypes.byref(wi), ctypes.byref(kpad), ctypes.byref(zr)))
+                                       ctypes.byref(wi), ctypes.byref(nwarps), ctypes.byref(kpad),
+                                       ctypes.byref(z0)))
         words = np.ctypeslib.as_array(ctypes.cast(w, ctypes.POINTER(ctypes.c_uint32)), (nw.value,)).copy()
-        info = np.ctypeslib.as_array(ctypes.cast(wi, ctypes.POINTER(ctypes.c_uint32)), (48,)).copy()
-        return words, cb.value, info.reshape(16, 3), kpad.value, zr.value
+        info = np.ctypeslib.as_array(ctypes.cast(wi, ctypes.POINTER(ctypes.c_uint32)),
+                                     (3 * nwarps.value,)).copy()
+        return words, cb.value, info.reshape(-1, 3), kpad.value, z0.value
 
     def set_variant(self, variant):
         _check(lib().fs_graph_set_variant(self._h, variant))
