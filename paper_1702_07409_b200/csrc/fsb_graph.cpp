@@ -227,6 +227,7 @@ void build_smem_schedule(Graph &g) {
   struct Pair {                      // one group: half 0 (A) and half 1 (B)
     uint16_t row[2] = {kNoRow, kNoRow};
     std::vector<uint16_t> seq[2];    // seq[0][e] even <=> seq[1][e] odd
+    bool split = false;              // pair-split: A and B hold the two parts of row[0]
   };
   struct Item {
     bool split = false;
@@ -266,8 +267,25 @@ void build_smem_schedule(Graph &g) {
 
   std::vector<Item> items;
   std::vector<uint32_t> light;
+  std::vector<Pair> pairs;
   for (uint32_t j = 0; j < n; ++j) {
     const uint32_t d = static_cast<uint32_t>(g.lt_row_ptr[j + 1] - g.lt_row_ptr[j]);
+    if (d > static_cast<uint32_t>(kSplitThreshold) && d <= static_cast<uint32_t>(kSplit2Max)) {
+      // pair-split: evens in half 0, odds in half 1 of one group
+      Pair pr;
+      pr.split = true;
+      pr.row[0] = static_cast<uint16_t>(j);
+      pr.row[1] = kNoRow;
+      std::vector<uint16_t> ev, od;
+      row_slots(j, ev, od);
+      const size_t L = std::max(ev.size(), od.size());
+      pr.seq[0] = ev;
+      pr.seq[1] = od;
+      pr.seq[0].resize(L, z0);
+      pr.seq[1].resize(L, z1);
+      pairs.push_back(std::move(pr));
+      continue;
+    }
     if (d > static_cast<uint32_t>(kSplitThreshold)) {
       Item it;
       it.split = true;
@@ -304,13 +322,38 @@ void build_smem_schedule(Graph &g) {
     if (degree(a) != degree(b)) return degree(a) > degree(b);
     return ecount[a] < ecount[b];
   });
-  std::vector<Pair> pairs;
+  // within a degree class d, a row with x even sources pairs best with one with d - x (its odds
+  // then meet the partner's evens one for one): exact complements first, then the extremes of
+  // what is left
   uint32_t carry = UINT32_MAX;  // an unpaired row left over from the previous class
   for (size_t c0 = 0; c0 < light.size();) {
     size_t c1 = c0;
     while (c1 < light.size() && degree(light[c1]) == degree(light[c0])) ++c1;
-    std::vector<uint32_t> cls(light.begin() + c0, light.begin() + c1);
-    if (carry != UINT32_MAX) cls.insert(cls.begin(), carry), carry = UINT32_MAX;
+    const uint32_t d = degree(light[c0]);
+    std::vector<std::vector<uint32_t>> by_x(d + 1);
+    for (size_t i = c0; i < c1; ++i) by_x[ecount[light[i]]].push_back(light[i]);
+    for (uint32_t x = 0; 2 * x <= d; ++x) {
+      std::vector<uint32_t> &a = by_x[x], &b = by_x[d - x];
+      if (x == d - x) {
+        while (a.size() >= 2) {
+          const uint32_t r0 = a.back();
+          a.pop_back();
+          const uint32_t r1 = a.back();
+          a.pop_back();
+          pairs.push_back(make_pair(r0, r1));
+        }
+      } else {
+        while (!a.empty() && !b.empty()) {
+          pairs.push_back(make_pair(a.back(), b.back()));
+          a.pop_back();
+          b.pop_back();
+        }
+      }
+    }
+    std::vector<uint32_t> cls;
+    if (carry != UINT32_MAX) cls.push_back(carry), carry = UINT32_MAX;
+    for (uint32_t x = 0; x <= d; ++x) cls.insert(cls.end(), by_x[x].begin(), by_x[x].end());
+    std::stable_sort(cls.begin(), cls.end(), [&](uint32_t a, uint32_t b) { return ecount[a] < ecount[b]; });
     size_t lo = 0, hi = cls.size();
     while (hi - lo >= 2) {
       pairs.push_back(make_pair(cls[lo], cls[hi - 1]));
@@ -376,6 +419,7 @@ void build_smem_schedule(Graph &g) {
     uint32_t steps = 0;
     for (uint32_t idx : per_warp[w]) {
       const Item &it = items[idx];
+      const bool item_pair_split = it.grp[0].split || it.grp[1].split || it.grp[2].split || it.grp[3].split;
       const size_t hb = heads.size();
       heads.resize(hb + wpc, 0);
       const uint32_t ncont = it.len > kHeadSlots ? (it.len - kHeadSlots + kChunkSlots - 1) / kChunkSlots : 0;
@@ -385,7 +429,10 @@ void build_smem_schedule(Graph &g) {
         const Pair &pr = it.grp[h >> 1];
         const std::vector<uint16_t> &seq = pr.seq[h & 1];
         heads[hb + h * 4] = static_cast<uint32_t>(pr.row[h & 1]) |
-                            (static_cast<uint32_t>(it.len | (it.split ? kSplitBit : 0)) << 16);
+                            (static_cast<uint32_t>(it.len | (it.split ? kSplitBit : 0) |
+                                                   (item_pair_split ? kPairSplitBit : 0))
+                             << 16);
+        if (pr.split) heads[hb + h * 4 + 1] |= kPairFlag;
         for (uint32_t e = 0; e < it.len; ++e) {
           if (seq[e] == z0 || seq[e] == z1) ++s.pad_slots;
           if (e < kHeadSlots) {

@@ -18,8 +18,9 @@ constexpr int kUnitBytes = kUnitRows * kSliceBytes;     // 4 KiB
 constexpr int kConsumerWarps = 20;
 constexpr int kHalvesPerWarp = 8;                        // half-groups: 4 lanes x 16 B = 64 B
 constexpr int kThreads = (kConsumerWarps + 1) * 32;      // + 1 producer warp (TMA + precode)
-constexpr int kSplitThreshold = 32;                      // rows of degree > this are split
-                                                         // over the 8 half-groups of a warp
+constexpr int kSplitThreshold = 48;                      // rows of degree > this are split:
+constexpr int kSplit2Max = 96;                           //   over the 2 halves of a group (<= this)
+                                                         //   or over the 8 half-groups of a warp
 
 // Bank rule: a 128-bit shared load is served in phases of 8 lanes = two half-groups (lanes
 // 8q..8q+3 = half 0, 8q+4..8q+7 = half 1).  A 64-B row r occupies the 16 banks of half (r & 1)
@@ -30,15 +31,18 @@ constexpr int kSplitThreshold = 32;                      // rows of degree > thi
 // Item-record schedule.  A warp's per-tile LT work is a list of *items*; an item gives each of
 // the warp's 8 half-groups one output row and the same number L of source slots.  A slot is an
 // 11-bit tile row (data m -> m, check i -> kpad+i, padding -> zero_even / zero_odd); two slots
-// share a 32-bit word as  a | b << 21  (bits 11..20 zero), so the kernel forms the shared
-// address of `b` with one shift-add (sbase + (w >> 15)).  Two streams, copied into shared
-// memory once per CTA, in 128-byte chunks (8 half-groups x 16 B; half-group g's 16 B at uint4
-// index chunk*8 + g):
+// share a 32-bit word as  a | b << 21  (bits 11..20 zero; bits 11..14 may carry flags, which the
+// address arithmetic ignores), so the kernel forms the shared address of `b` with one shift-add
+// (sbase + (w >> 15)).  Two streams, copied into shared memory once per CTA, in 128-byte chunks
+// (8 half-groups x 16 B; half-group g's 16 B at uint4 index chunk*8 + g):
 //   heads: one chunk per item: word 0 = row | ctrl << 16, words 1..3 = slots 0..5; ctrl =
-//          L | split<<15 (identical in all 8 half-groups); row = kNoRow for an unused half;
+//          L | pair-split << 14 | warp-split << 15 (identical in all 8 half-groups); row =
+//          kNoRow for a half-group that stores nothing; word 1 bit 11 (kPairFlag) marks a
+//          half-group whose partner half holds the other part of the same row;
 //   conts: slots 6.. of items with L > 6, 8 per chunk (4 words), items in the same order.
-// A split item spreads one heavy row over the 8 half-groups (evens to half 0, odds to half 1),
-// which then combine their partial XORs with three warp shuffles (same row in all 8).
+// Heavy rows: degree <= kSplit2Max -> a pair-split: evens in half 0, odds in half 1 of one group
+// (combined by one xor-4 warp shuffle, stored by half 0); larger -> a warp-split item: evens over
+// the four half-0, odds over the four half-1 half-groups (three warp shuffles, same row in all 8).
 constexpr uint32_t kHeadSlots = 6;          // slots in an item's head chunk
 constexpr uint32_t kChunkSlots = 8;         // slots in a continuation chunk
 constexpr uint32_t kChunkBytes = kHalvesPerWarp * 16;
@@ -46,8 +50,10 @@ constexpr uint32_t kStreamPad = 2;          // zero chunks after each stream (pr
 constexpr uint32_t kSlotBits = 11;
 constexpr uint32_t kSlotHiShift = 21;
 constexpr uint16_t kNoRow = 0xFFFF;
-constexpr uint16_t kSplitBit = 0x8000;
-constexpr uint32_t kMaxItemLen = 0x7FFF;
+constexpr uint16_t kSplitBit = 0x8000;       // ctrl: warp-split item
+constexpr uint16_t kPairSplitBit = 0x4000;   // ctrl: the item holds pair-split groups
+constexpr uint32_t kPairFlag = 1u << 11;     // head word 1: this half-group's pair is split
+constexpr uint32_t kMaxItemLen = 0x3FFF;
 constexpr uint32_t kMaxSmemRows = 0xFFFE;   // n limit of the SMEM variant (16-bit output rows)
 constexpr uint32_t kMaxSmemSlots = (1u << kSlotBits) - 1;  // tile rows (data + checks + zero rows)
 

@@ -174,7 +174,7 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
     }
     gather_xor_n<0>(acc, c, rem, sbase);
   }
-  if (ctrl & kSplitBit) {  // split row: combine the eight half-groups' partial XORs
+  if (ctrl & kSplitBit) {  // warp-split row: combine the eight half-groups' partial XORs
 #pragma unroll
     for (int o = 4; o <= 16; o <<= 1) {
       acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -183,9 +183,17 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
       acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, o);
     }
     if (half_id == 0) st_stream(out + static_cast<uint64_t>(row) * t, acc);
-  } else if (row != kNoRow) {
-    st_stream(out + static_cast<uint64_t>(row) * t, acc);
+    return;
   }
+  if (ctrl & kPairSplitBit) {  // pair-split groups: half 0 takes its partner half's part
+    uint4 o;
+    o.x = __shfl_xor_sync(0xffffffffu, acc.x, 4);
+    o.y = __shfl_xor_sync(0xffffffffu, acc.y, 4);
+    o.z = __shfl_xor_sync(0xffffffffu, acc.z, 4);
+    o.w = __shfl_xor_sync(0xffffffffu, acc.w, 4);
+    if (h.y & kPairFlag) xor_into(acc, o);
+  }
+  if (row != kNoRow) st_stream(out + static_cast<uint64_t>(row) * t, acc);
 }
 
 // Persistent encode kernel, one CTA per SM.  Shared memory: two tile buffers (tile_units x 4 KiB

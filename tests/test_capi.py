@@ -175,11 +175,15 @@ def _simulate_schedule(g, c):
             head = heads[hpos]
             hslots = head_slots[hpos]
             hpos += 1
-            assert all(((int(head[h, j]) >> 11) & 0x3FF) == 0 for h in range(8) for j in (1, 2, 3))
+            pflag = [bool(int(head[h, 1]) & (1 << 11)) for h in range(8)]
+            # bits 11..20 of slot words are zero, except the pair-split flag (word 1, bit 11)
+            assert all(((int(head[h, j]) >> 11) & 0x3FF) == (1 if j == 1 and pflag[h] else 0)
+                       for h in range(8) for j in (1, 2, 3))
             ctrls = set(int(head[h, 0]) >> 16 for h in range(8))
             assert len(ctrls) == 1, "non-uniform item control"
             ctrl = ctrls.pop()
-            L, split = ctrl & 0x7FFF, bool(ctrl & 0x8000)
+            L, split, psplit = ctrl & 0x3FFF, bool(ctrl & 0x8000), bool(ctrl & 0x4000)
+            assert psplit == any(pflag)
             assert L >= 1
             per = [[] for _ in range(8)]
             for e in range(L):
@@ -197,6 +201,11 @@ def _simulate_schedule(g, c):
                     assert (vals[2 * q] & 1) != (vals[2 * q + 1] & 1), "bank rule"
             cpos += 0 if L <= 6 else (L - 6 + 7) // 8
             outs = [int(head[h, 0]) & 0xFFFF for h in range(8)]
+            for q in range(4):   # pair-split: half 0 stores both halves' parts
+                if pflag[2 * q]:
+                    assert pflag[2 * q + 1] and outs[2 * q + 1] == 0xFFFF and outs[2 * q] != 0xFFFF
+                    per[2 * q] = per[2 * q] + per[2 * q + 1]
+                    per[2 * q + 1] = []
             if split:
                 assert len(set(outs)) == 1 and outs[0] != 0xFFFF
                 assert outs[0] not in rows
