@@ -2,21 +2,25 @@
 """Benchmark of the Founsure encode hot path on B200 (BASELINE.json metric: encode throughput,
 source GB/s, % of HBM roofline).
 
-Workload: BASELINE config 4 -- 256 independent stripes of k=1024 x t=4096 B
-(1 GiB of seeded uniform bytes), precode p=16 checks of degree 3, n=1280 coded symbols with
-RSD(c=0.1, delta=0.05) -- per GPU (weak scaling: each rank encodes its own 1 GiB shard of the
-same stream; --scaling strong splits one 1 GiB file instead).  One step = one pass of the
-whole hot path (precode + LT over every stripe) = one fs_encode_stripes call.
+Workload: BASELINE config 4 -- 1 GiB of seeded uniform bytes split into 256
+independent stripes of k=1024 x t=4096 B, precode p=16 checks of degree 3, n=1280 coded symbols
+with RSD(c=0.1, delta=0.05).  One step = one pass of the whole hot path (precode + LT over every
+stripe of the rank's shard) = one fs_encode_stripes call.  `--scaling strong` (default) shards the
+256 stripes over the ranks as BASELINE config 4 states; `--scaling weak` gives every rank its own
+1 GiB.  `--config 5` (one 410 MB stripe) partitions the coded rows over the ranks with the source
+replicated (reading R16); other configs run on one GPU.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
-N > 1 runs under torchrun (one process per GPU, NCCL); the graph is generated on rank 0 and
-broadcast over NCCL, stripes are sharded with no data-path collective, the time is the max
-over ranks of the CUDA-event time of K steps.  Rank 0 prints one JSON line.
+N > 1 runs under torchrun (one process per GPU, NCCL): the graph is generated on rank 0 and
+broadcast over NCCL (paper_1702_07409_b200/dist.py), work is sharded with no data-path
+collective, and the time is the max over ranks of the CUDA-event time of K steps.  Rank 0 prints
+one JSON line.
 """
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -27,13 +31,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_1702_07409_b200 import configs, fsb, inputs  # noqa: E402
+from paper_1702_07409_b200 import configs, dist as fdist, fsb, inputs  # noqa: E402
 
 METRIC = "encode throughput, source GB/s (1/2/4/8 B200), % of HBM roofline"
-SMEM_GATHER_PEAK_GBS = 36806.0   # measured: tools/microbench/mb.cu smem_gather (profiles/microbench_r01.md)
+DATA = "synthetic: seeded counter-form splitmix64 bytes (DESIGN.md R4), graph seed = data seed (R3)"
+# Shared-memory gather peak for the secondary (gather-traffic) roofline: parity-paired 64-B row
+# gathers, 122 B/clk/SM at 1965 MHz x 148 SMs (tools/microbench/mb3.cu, profiles/r01b/).
+SMEM_GATHER_PEAK_GBS = 35595.0
 REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
 
@@ -45,6 +51,19 @@ def _peaks():
         return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _host_cpu():
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
 
 
 class ClockSampler:
@@ -105,34 +124,16 @@ def _dist_env():
     return ws, rank, local
 
 
-def _shard(args, cfg, ws, rank):
+def plan(cfg, ws, rank, scaling):
+    """This rank's work: ("stripes", first stripe, count) or ("rows", row_begin, row_end)."""
     S_total = cfg["stripes"]
-    if args.scaling == "weak":
-        return rank * S_total, S_total          # each rank: its own full-size shard
-    a, b = rank * S_total // ws, (rank + 1) * S_total // ws
-    return a, b - a
-
-
-def _graph(cfg, ws, rank, dev):
-    """Rank 0 generates; other ranks receive the CSR over NCCL (step a2)."""
-    if ws == 1:
-        return fsb.Graph.create(cfg)
-    import torch.distributed as dist
-    if rank == 0:
-        g = fsb.Graph.create(cfg)
-        arrs = g.csr()
-        sizes = torch.tensor([len(a) for a in arrs], dtype=torch.int64, device=dev)
-    else:
-        sizes = torch.zeros(4, dtype=torch.int64, device=dev)
-    dist.broadcast(sizes, 0)
-    bufs = []
-    for i, n in enumerate(sizes.tolist()):
-        t = torch.from_numpy(arrs[i]).to(dev) if rank == 0 else torch.empty(n, dtype=torch.int32, device=dev)
-        dist.broadcast(t, 0)
-        bufs.append(t.cpu().numpy())
-    if rank == 0:
-        return g
-    return fsb.Graph.from_csr(cfg, *bufs)
+    if S_total == 1 and ws > 1:
+        r0, r1 = fdist.shard(cfg["n"], ws, rank)
+        return "rows", r0, r1
+    if scaling == "weak":
+        return "stripes", rank * S_total, S_total
+    a, b = fdist.shard(S_total, ws, rank)
+    return "stripes", a, b - a
 
 
 def cpu_oracle_sample(cfg, seconds, max_stripes=None):
@@ -149,17 +150,21 @@ def cpu_oracle_sample(cfg, seconds, max_stripes=None):
         t_enc += time.perf_counter() - t0
         done += 1
     src = done * cfg["k"] * cfg["t"]
+    host = _host_cpu()
     return {"value": src / t_enc / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": "%d of %d stripes of %s (%.1f MB source), single-threaded C oracle, %.1f s"
+            "host_cpu": host["model"], "host_nproc": host["nproc"],
+            "sample": "%d of %d stripes of %s (%.1f MB source), single-threaded C oracle, %.2f s"
                       % (done, S, cfg["name"], src / 1e6, t_enc)}
 
 
 def run_reference(args, cfg):
+    """Reference arm for this tier: the CPU oracle timed as it stands on the host cores, on the
+    same config, metric and unit; rank 0 only, the whole run bounded by --ref-seconds."""
     ws, rank, _ = _dist_env()
     if rank != 0:
         return
     steps, warm = args.steps, args.warmup
-    per_step = max(0.5, args.ref_seconds / max(1, steps))
+    per_step = args.ref_seconds / max(1, steps)
     for _ in range(warm):
         cpu_oracle_sample(cfg, 0.0, max_stripes=1)
     vals = [cpu_oracle_sample(cfg, per_step) for _ in range(steps)]
@@ -169,9 +174,9 @@ def run_reference(args, cfg):
     cb["sample"] = "per step: " + vals[0]["sample"]
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
            "steps": steps, "warmup": warm, "higher_is_better": True, "scaling": args.scaling,
-           "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded splitmix64 bytes, DESIGN.md R4)",
+           "vs_baseline": None, "dtype": "u8", "data": DATA,
            "config": {"workload": cfg["name"], "k": cfg["k"], "p": cfg["p"], "n": cfg["n"],
-                      "t": cfg["t"], "stripes_per_gpu": cfg["stripes"]},
+                      "t": cfg["t"], "stripes": cfg["stripes"]},
            "cpu_baseline": cb,
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
@@ -184,7 +189,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
     ap.add_argument("--variant", default="auto", choices=["auto", "smem", "global"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -204,19 +209,29 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    g = _graph(cfg, ws, rank, dev)
+        g = fdist.broadcast_graph(cfg, device=dev)        # step a2 over NCCL
+    else:
+        g = fsb.Graph.create(cfg)
     if args.variant != "auto":
         g.set_variant(fsb.VARIANT_SMEM if args.variant == "smem" else fsb.VARIANT_GLOBAL)
-    s0, S = _shard(args, cfg, ws, rank)
+    kind, u0, u1 = plan(cfg, ws, rank, args.scaling)
     k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
-    data = inputs.stripe_data(cfg, stripe_begin=s0, num_stripes=S, device=dev)
+    if kind == "stripes":
+        S, rows = u1, n
+        data = inputs.stripe_data(cfg, stripe_begin=u0, num_stripes=S, device=dev)
+    else:
+        S, rows = 1, u1 - u0
+        data = inputs.stripe_data(cfg, device=dev)       # the source is replicated (R16)
     chk = torch.empty((S, p, t), dtype=torch.uint8, device=dev) if p else None
-    cod = torch.empty((S, n, t), dtype=torch.uint8, device=dev)
+    cod = torch.empty((S, rows, t), dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
 
     def step():
-        g.encode_stripes(data, chk, cod, stream=stream)
+        if kind == "stripes":
+            g.encode_stripes(data, chk, cod, stream=stream)
+        else:
+            g.encode(data[0], chk[0] if p else None, cod[0], u0, u1, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -236,56 +251,64 @@ def main():
             evs[i + 1].record(stream)
     stream.synchronize()
     torch.cuda.synchronize()
-    clk = clocks.stop()
-    total_ms = evs[0].elapsed_time(evs[-1])
-    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
-    t_max = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if ws > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
         dist.barrier()
-    total_ms = float(t_max.item())
+    clk = clocks.stop()
+    my_ms = evs[0].elapsed_time(evs[-1])
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    total_ms = fdist.max_over_ranks(my_ms, device=dev) if ws > 1 else my_ms
     ms_per_step = total_ms / args.steps
-    src_bytes_all = ws * S * k * t if args.scaling == "weak" else cfg["stripes"] * k * t
+    if kind == "stripes":
+        src_bytes_all = (ws * S if args.scaling == "weak" else cfg["stripes"]) * k * t
+    else:
+        src_bytes_all = k * t                                # one stripe, rows split over ranks
     value = src_bytes_all / (ms_per_step * 1e-3) / 1e9
 
-    # roofline of the dominant kernel: algorithmic HBM bytes per launch / mean launch time
+    # roofline of the dominant kernel (this rank): algorithmic HBM bytes per launch (one read of
+    # the source, one write of checks + coded rows) / mean step time on the stream
     inf = g.info()
-    b_hbm = S * (k + p + n) * t
-    b_gather = S * ((inf["lt_nnz"] + inf["pre_nnz"]) * t)
+    b_hbm = S * (k + p + rows) * t
+    b_gather = S * (inf["lt_nnz"] * rows // n + inf["pre_nnz"]) * t
     launch_ms = statistics.mean(per)
     peak, peak_src = _peaks()
     achieved = b_hbm / (launch_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and kind == "stripes" and S == cfg["stripes"]:
         try:
             traffic = json.load(open(tp)).get(cfg["name"], {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    smem_kernel = launches_per_step == 1
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
             "algorithmic_bytes_per_launch": b_hbm, "peak_source": peak_src,
-            "kernel": "fsb_smem_encode" if launches_per_step == 1 else "fsb_precode_global+fsb_lt_global",
+            "kernel": "fsb_smem_encode" if smem_kernel else "fsb_precode_global+fsb_lt_global",
+            "timing": "CUDA events on the launching stream, mean per step (%d launch%s per step)"
+                      % (launches_per_step, "" if smem_kernel else "es"),
             "gather": {"bytes_per_launch": b_gather,
                        "achieved": round(b_gather / (launch_ms * 1e-3) / 1e9, 1),
                        "peak": SMEM_GATHER_PEAK_GBS, "unit": "GB/s",
                        "frac": round(b_gather / (launch_ms * 1e-3) / 1e9 / SMEM_GATHER_PEAK_GBS, 4),
-                       "peak_source": "measured smem random-row gather, tools/microbench/mb.cu"}}
+                       "peak_source": "measured parity-paired 64-B smem row gather, tools/microbench/mb3.cu"}}
 
-    # e2e: host (pinned) buffers through the public API, copies inside the timed region
     e2e = None
-    if args.e2e_steps > 0:
-        e2e = _e2e(g, cfg, data, cod, S, args, dev, ws)
+    if args.e2e_steps > 0 and kind == "stripes":
+        e2e = _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all)
 
     out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-           "scaling": args.scaling, "vs_baseline": None, "dtype": "u8",
-           "data": "synthetic (seeded splitmix64 bytes, DESIGN.md R4)",
+           "scaling": args.scaling if kind == "stripes" else "strong", "vs_baseline": None, "dtype": "u8",
+           "data": DATA,
            "config": {"workload": cfg["name"], "k": k, "p": p, "d_p": cfg["d_p"], "n": n, "t": t,
-                      "dist": "RSD" if cfg["dist"] == configs.RSD else "Omega", "stripes_per_gpu": S,
-                      "stripes_total": S * ws if args.scaling == "weak" else cfg["stripes"],
-                      "parallelism": "stripe-sharded x%d" % ws, "variant": args.variant,
-                      "l2": "inputs (%.2f GB) exceed the 126 MB L2; no flush needed" % (S * k * t / 1e9),
+                      "dist": "RSD" if cfg["dist"] == configs.RSD else "Omega",
+                      "stripes_total": cfg["stripes"] * (ws if args.scaling == "weak" and kind == "stripes" else 1),
+                      "per_rank": ("%d stripes" % S) if kind == "stripes" else ("rows [%d,%d)" % (u0, u1)),
+                      "parallelism": ("stripe-sharded x%d" % ws) if kind == "stripes" else
+                                     ("coded-row partition x%d, source replicated" % ws),
+                      "variant": args.variant,
+                      "l2": "inputs (%.2f GB per rank) exceed the 126 MB L2; no flush needed"
+                            % (S * k * t / 1e9),
                       "lt_nnz": inf["lt_nnz"], "max_degree": inf["max_degree"]},
            "roofline": roof, "gpu_launches": launches_per_step * args.steps,
            "step_ms_median": round(statistics.median(per), 5), "clocks": clk, "e2e": e2e}
@@ -297,10 +320,10 @@ def main():
         dist.destroy_process_group()
 
 
-def _e2e(g, cfg, data, cod, S, args, dev, ws):
+def _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all):
     """Same metric through fs_encode_stripes with HOST buffers: per step, H2D of the step's
     data from pinned memory, the encode, and D2H of checks + coded, pipelined over chunks of
-    stripes on two streams."""
+    stripes on two streams (copies overlap the kernels of neighbouring chunks)."""
     k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
     h_data = torch.empty((S, k, t), dtype=torch.uint8, pin_memory=True)
     h_data.copy_(data.cpu())
@@ -344,17 +367,13 @@ def _e2e(g, cfg, data, cod, S, args, dev, ws):
     e1.record(cur)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    tm = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    ms = float(tm.item()) / args.e2e_steps
+    ms = (fdist.max_over_ranks(ms, device=dev) if ws > 1 else ms) / args.e2e_steps
     # spot-check the host result against the device-resident run
     ok = bool(torch.equal(h_cod[0].to(dev), cod[0]) and torch.equal(h_cod[S - 1].to(dev), cod[S - 1]))
-    return {"value": round(ws * S * k * t / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+    return {"value": round(src_bytes_all / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": S * k * t, "d2h_bytes_per_step": S * (p + n) * t,
-            "ms_per_step": round(ms, 3), "api": "fs_encode_stripes on pinned-host staging, %d chunks x 2 streams"
-            % nchunks, "checked": ok}
+            "ms_per_step": round(ms, 3),
+            "api": "fs_encode_stripes on pinned-host staging, %d chunks x 2 streams" % nchunks, "checked": ok}
 
 
 if __name__ == "__main__":

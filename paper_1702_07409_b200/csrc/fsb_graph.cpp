@@ -381,7 +381,13 @@ void build_smem_schedule(Graph &g) {
   for (const Item &it : items)
     if (it.len > kMaxItemLen || it.len == 0) return;
   // LPT over warps; cost ~ gather steps + per-item overhead (head, dispatch, store)
-  auto cost = [](const Item &it) { return it.len + (it.split ? 8u : 6u); };
+  // LPT cost of an item in gather steps: L plus a per-item overhead (head load, dispatch, store);
+  // FSB_ITEM_OVERHEAD overrides it (tuning experiments)
+  static const uint32_t overhead = [] {
+    const char *e = std::getenv("FSB_ITEM_OVERHEAD");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 6u;
+  }();
+  auto cost = [](const Item &it) { return it.len + overhead + (it.split ? 2u : 0u); };
   std::vector<uint32_t> order(items.size());
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost(items[a]) > cost(items[b]); });

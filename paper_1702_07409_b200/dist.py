@@ -1,0 +1,58 @@
+"""Multi-GPU plumbing of the encode path -- host logic only.
+
+One process per GPU.  The units of work are independent: stripes ("partitions are
+processed independent of each other") for multi-stripe encodes, or coded-row ranges of one stripe
+(reading R16) for a single large stripe.  The only collective is step a2: rank 0 generates the
+graph (fs_graph_create) and broadcasts its CSR; the other ranks rebuild it with
+fs_graph_from_csr.  There is no data-path collective.
+
+Works with any torch.distributed backend: NCCL (device tensors) on the GPU box, gloo (CPU
+tensors) in the CPU tests.
+"""
+import numpy as np
+import torch
+
+from . import fsb
+
+
+def shard(total, world_size, rank):
+    """Contiguous [begin, end) share of `total` units for `rank` (sizes differ by at most 1)."""
+    if world_size < 1 or not 0 <= rank < world_size:
+        raise ValueError("bad world_size / rank")
+    return rank * total // world_size, (rank + 1) * total // world_size
+
+
+def broadcast_graph(cfg, group=None, device="cpu", host_only=False):
+    """Step a2: rank 0 generates the graph, every rank returns an fsb.Graph with identical CSR.
+
+    The four int32 CSR arrays travel as one flat tensor (one size broadcast, one data
+    broadcast) on `device` (a CUDA device for NCCL, "cpu" for gloo)."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    if rank == 0:
+        g = fsb.Graph.create(cfg, host_only=host_only)
+        arrs = g.csr()
+        sizes = torch.tensor([len(a) for a in arrs], dtype=torch.int64, device=device)
+    else:
+        g, arrs = None, None
+        sizes = torch.zeros(4, dtype=torch.int64, device=device)
+    dist.broadcast(sizes, 0, group=group)
+    n = [int(x) for x in sizes.tolist()]
+    if rank == 0:
+        flat = torch.from_numpy(np.concatenate(arrs).astype(np.int32)).to(device)
+    else:
+        flat = torch.empty(sum(n), dtype=torch.int32, device=device)
+    dist.broadcast(flat, 0, group=group)
+    if rank == 0:
+        return g
+    host = flat.cpu().numpy()
+    parts = np.split(host, np.cumsum(n)[:-1])
+    return fsb.Graph.from_csr(cfg, *parts, host_only=host_only)
+
+
+def max_over_ranks(value, group=None, device="cpu"):
+    """The max of a float over all ranks (the bench's timing rule)."""
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

@@ -1,0 +1,96 @@
+"""Multi-GPU host logic on CPU: world_size-2 gloo process groups.
+
+Covers step a2 (rank 0 generates the graph, the CSR is broadcast, the other ranks rebuild it with
+fs_graph_from_csr), the max-over-ranks timing reduction, and bench.py's work partition (stripes
+for multi-stripe configs, coded rows for a single stripe).  No GPU is touched: graphs are
+host-only.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from paper_1702_07409_b200 import configs, dist as fdist, fsb  # noqa: E402
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, ws, port, cid, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=ws)
+        cfg = configs.get(cid)
+        g = fdist.broadcast_graph(cfg, device="cpu", host_only=True)
+        local = fsb.Graph.create(cfg, host_only=True)      # independent regeneration
+        same = all(np.array_equal(a, b) for a, b in zip(g.csr(), local.csr()))
+        t = fdist.max_over_ranks(1.5 + rank, device="cpu")
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, same, t, g.info()["lt_nnz"]))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, "error", repr(e), None))
+
+
+@pytest.mark.parametrize("cid", [2, 4])
+def test_graph_broadcast_gloo_world2(cid):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, cid, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    res.sort()
+    for rank, same, t, nnz in res:
+        assert same is True, (rank, same, t)
+        assert t == 2.5                                     # max over ranks
+    assert res[0][3] == res[1][3]
+
+
+def test_shard_covers_exactly_once():
+    for total in (0, 1, 7, 256, 60000):
+        for ws in (1, 2, 3, 4, 8):
+            seen = []
+            for r in range(ws):
+                a, b = fdist.shard(total, ws, r)
+                assert 0 <= a <= b <= total
+                assert b - a in (total // ws, total // ws + 1)
+                seen.extend(range(a, b))
+            assert seen == list(range(total))
+    with pytest.raises(ValueError):
+        fdist.shard(10, 2, 2)
+
+
+def test_bench_plan():
+    import bench
+    c4, c5 = configs.get(4), configs.get(5)
+    for ws in (1, 2, 4, 8):
+        stripes = [bench.plan(c4, ws, r, "strong") for r in range(ws)]
+        assert all(k == "stripes" for k, _, _ in stripes)
+        assert sum(cnt for _, _, cnt in stripes) == c4["stripes"]
+        assert [s0 for _, s0, _ in stripes] == sorted(s0 for _, s0, _ in stripes)
+        weak = [bench.plan(c4, ws, r, "weak") for r in range(ws)]
+        assert all(cnt == c4["stripes"] and s0 == r * c4["stripes"] for r, (_, s0, cnt) in enumerate(weak))
+        rows = [bench.plan(c5, ws, r, "strong") for r in range(ws)]
+        if ws == 1:
+            assert rows == [("stripes", 0, 1)]
+        else:
+            assert all(k == "rows" for k, _, _ in rows)
+            assert rows[0][1] == 0 and rows[-1][2] == c5["n"]
+            assert all(rows[i][2] == rows[i + 1][1] for i in range(ws - 1))

@@ -2,7 +2,12 @@
 // Every variant does parity-paired 64-B row gathers (conflict-free, measured in mb3.cu) and adds
 // one op per 8 gathers: 1 schedule-chunk load (half-group h reads 16-B word h of a 128-B chunk),
 // 2 warp shuffles (xor 4), 3 a 16-B global store per lane, 4 all lanes gather the same 2 rows,
-// 5 gathers where the 4 groups read the same even/odd row pair (cross-phase duplicates).
+// 5 gathers where the 4 groups read the same even/odd row pair (cross-phase duplicates),
+// 6 a 16-B global store per lane where each half-group (4 lanes, 64 B) writes its own 4-KB-strided
+//   row (8 distinct 128-B lines per store, the SMEM kernel's coded-row store),
+// 7 as 6 but each group (8 lanes, 128 B) writes one full line (4 lines per store),
+// 8 as 6 but staged: each half-group writes its 64 B to a per-warp shared staging slot (STS) and
+//   lane 4h issues a 64-B cp.async.bulk shared->global copy of it (double-buffered staging).
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -10,6 +15,7 @@
 template <int V>
 __global__ void __launch_bounds__(512, 1) mix(uint4* out, int rows, int iters) {
   extern __shared__ uint4 sm[];
+  __shared__ __align__(128) uint4 stage[16][2][32];  // warp, buffer, 8 half-groups x 4 lanes
   for (int i = threadIdx.x; i < rows * 4; i += blockDim.x) sm[i] = make_uint4(i, i * 3, i * 7, i * 11);
   __syncthreads();
   const int lane = threadIdx.x & 31, lane4 = lane & 3, half = (lane >> 2) & 1;
@@ -37,7 +43,31 @@ __global__ void __launch_bounds__(512, 1) mix(uint4* out, int rows, int iters) {
       acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, 4);
     }
     if (V == 3) out[(blockIdx.x * blockDim.x + threadIdx.x + it * 64) & (1024 * 512 - 1)] = acc;
+    if (V == 6) {
+      const uint32_t row = (hw + (threadIdx.x >> 2) * 7919u) & 2047u;  // 2048 rows of 4 KB
+      out[(row * 256 + blockIdx.x * 4 + lane4) & (1024 * 512 - 1)] = acc;
+    }
+    if (V == 8) {
+      const uint32_t w = threadIdx.x >> 5, buf = it & 1;
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer `buf` reusable
+      __syncwarp();
+      stage[w][buf][lane] = acc;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane4 == 0) {
+        const uint32_t row = (hw + (threadIdx.x >> 2) * 7919u) & 2047u;
+        uint4* dst = out + ((row * 256 + blockIdx.x * 4) & (1024 * 512 - 1));
+        const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(&stage[w][buf][lane]));
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 64;" ::"l"(dst), "r"(src) : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    if (V == 7) {
+      const uint32_t row = (hw + (threadIdx.x >> 3) * 7919u) & 2047u;
+      out[(row * 256 + blockIdx.x * 8 + (lane & 7)) & (1024 * 512 - 1)] = acc;
+    }
   }
+  if (V == 8) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
@@ -63,6 +93,7 @@ void run(uint4* out, int sms) {
 int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   uint4* out; cudaMalloc(&out, 1024 * 512 * 16);
-  run<0>(out, sms); run<1>(out, sms); run<2>(out, sms); run<3>(out, sms); run<4>(out, sms); run<5>(out, sms);
+  run<0>(out, sms); run<1>(out, sms); run<2>(out, sms); run<3>(out, sms); run<5>(out, sms);
+  run<6>(out, sms); run<7>(out, sms); run<8>(out, sms);
   return 0;
 }
