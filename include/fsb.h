@@ -69,7 +69,7 @@ typedef struct {
   uint32_t p;             /* precode checks (paper k-b); 0 = no precode                       */
   uint32_t d_p;           /* data neighbours per check; 1 <= d_p <= k when p > 0             */
   uint32_t n;             /* coded symbols; >= 1                                              */
-  uint64_t t;             /* bytes per symbol; multiple of 16                                 */
+  uint64_t t;             /* bytes per symbol; multiple of 16, below 2^31                     */
   int32_t dist;           /* fs_dist_kind                                                     */
   double rsd_c;           /* RSD: c > 0                                                       */
   double rsd_delta;       /* RSD: 0 < delta < 1                                               */
@@ -94,7 +94,7 @@ typedef struct fs_graph fs_graph;  /* opaque */
 /* Seeded graph generation (step a1): precode rows first, then LT rows (reading R5), each
  * neighbour list sorted ascending (R14).  Without FS_GRAPH_HOST_ONLY the CSR and the work
  * schedules are uploaded to the current device (synchronously, before return).
- * FS_EINVAL: k == 0, n == 0, t == 0 or t % 16 != 0, p > 0 with d_p == 0 or d_p > k,
+ * FS_EINVAL: k == 0, n == 0, t == 0, t % 16 != 0 or t >= 2^31, p > 0 with d_p == 0 or d_p > k,
  *            K = k+p >= 2^31.
  * FS_EDIST:  empty support, degree 0, degrees not strictly increasing, negative weight,
  *            |sum - 1| > 1e-5, RSD c <= 0, delta outside (0,1), R/delta <= 1, K/R < 1.   */

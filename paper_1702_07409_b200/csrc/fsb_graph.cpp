@@ -58,6 +58,7 @@ struct NeighbourSampler {
 fs_status validate_params(const fs_params &prm) {
   if (prm.k == 0 || prm.n == 0) { set_error("k and n must be >= 1"); return FS_EINVAL; }
   if (prm.t == 0 || prm.t % 16 != 0) { set_error("t must be a positive multiple of 16"); return FS_EINVAL; }
+  if (prm.t >= (1ull << 31)) { set_error("t must be below 2^31"); return FS_EINVAL; }
   if (prm.p > 0 && (prm.d_p == 0 || prm.d_p > prm.k)) {
     set_error("precode degree d_p must satisfy 1 <= d_p <= k");
     return FS_EINVAL;

@@ -18,7 +18,7 @@
 //       aware schedule (fsb_graph.cpp): heavy rows are split over the 4 lane-groups of a
 //       warp and recombined with shuffles; light rows are packed by equal degree.
 //
-// GLOBAL (fsb_precode_global + fsb_lt_global): no staging; every group of 8 lanes XORs one
+// GLOBAL (fsb_precode_global + fsb_lt_band): no staging; every group of 8 lanes XORs one
 //       (row, 128-B slice) by 16-B loads from global memory, with the launch rasterised
 //       band-major (512-B bands of the symbols) so the band of the source block stays
 //       resident in L2 while every row consumes it.  Used for single large stripes
@@ -303,7 +303,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kGlobalThreads = 256;
 constexpr int kGroupsPerBlock = kGlobalThreads / 8;
 constexpr uint32_t kGSliceBytes = 128;  // one 8-lane group = 8 x 16 B
-constexpr uint32_t kBandSlices = 4;    // 512-B bands: one warp = one row x 4 slices
 
 __global__ void __launch_bounds__(kGlobalThreads)
     fsb_precode_global(uint32_t S, uint32_t p, uint32_t d_p, uint64_t t, uint32_t nslices,
@@ -328,45 +327,74 @@ __global__ void __launch_bounds__(kGlobalThreads)
   *reinterpret_cast<uint4 *>(checks + s * checks_stride + static_cast<uint64_t>(c) * t + byte) = acc;
 }
 
-__global__ void __launch_bounds__(kGlobalThreads)
-    fsb_lt_global(uint32_t S, uint32_t k, uint64_t t, uint32_t nslices, uint32_t nbands,
-                  uint32_t row_begin, uint32_t nrows, const int32_t *__restrict__ row_ptr,
-                  const int32_t *__restrict__ col, const uint8_t *__restrict__ data, uint64_t data_stride,
-                  const uint8_t *__restrict__ checks, uint64_t checks_stride, uint8_t *__restrict__ coded,
-                  uint64_t coded_stride) {
-  uint64_t e = static_cast<uint64_t>(blockIdx.x) * kGroupsPerBlock + (threadIdx.x >> 3);
-  const uint32_t lane8 = threadIdx.x & 7;
-  const uint32_t q = e % kBandSlices;
-  e /= kBandSlices;
-  const uint32_t jr = e % nrows;
-  e /= nrows;
-  const uint32_t band = e % nbands;
-  const uint64_t s = e / nbands;
+// LT rows of one (stripe, 512-B band) per warp and chunk of kBandRows consecutive coded rows.
+// Lane l owns bytes [band*512 + 16l, +16) of every row.  The chunk's CSR column indices are read
+// 32 at a time with one coalesced load and broadcast by shuffles, so the 512-B source gathers
+// (16 B per lane, 4 full lines per warp load) are independent of any other global load and go out
+// kBandBatch at a time.  Warps are ordered band-major (the unit index runs over chunks fastest),
+// so all SMs sweep the same band of the source block, which stays resident in L2 (config 5: a
+// 512-B band of all 50,500 rows is 25.9 MB) while every coded row consumes it: HBM reads the
+// source about once, the gathers hit L2.
+constexpr uint32_t kBandBytes = 512;
+constexpr uint32_t kBandRowsMax = 8;   // coded rows per warp (fewer when the call is small)
+constexpr uint32_t kBandBatch = 8;
+
+__global__ void __launch_bounds__(kGlobalThreads, 4)
+    fsb_lt_band(uint32_t S, uint32_t k, uint32_t t, uint32_t nbands, uint32_t row_begin, uint32_t nrows,
+                uint32_t band_rows, const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                const uint8_t *__restrict__ data, uint64_t data_stride, const uint8_t *__restrict__ checks,
+                uint64_t checks_stride, uint8_t *__restrict__ coded, uint64_t coded_stride) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nchunks = (nrows + band_rows - 1) / band_rows;
+  uint64_t unit = static_cast<uint64_t>(blockIdx.x) * (kGlobalThreads / 32) + (threadIdx.x >> 5);
+  const uint32_t chunk = static_cast<uint32_t>(unit % nchunks);
+  unit /= nchunks;
+  const uint32_t band = static_cast<uint32_t>(unit % nbands);
+  const uint64_t s = unit / nbands;
   if (s >= S) return;
-  const uint32_t slice = band * kBandSlices + q;
-  const uint64_t byte = static_cast<uint64_t>(slice) * kGSliceBytes + lane8 * 16;
-  if (slice >= nslices || byte >= t) return;
-  const uint32_t j = row_begin + jr;
-  const uint8_t *dsrc = data + s * data_stride + byte;
-  const uint8_t *csrc = checks + s * checks_stride + byte;
-  int32_t b = __ldg(&row_ptr[j]);
-  const int32_t end = __ldg(&row_ptr[j + 1]);
+  const uint32_t byte_raw = band * kBandBytes + lane * 16;
+  const bool active = byte_raw < t;                   // ragged last band
+  const uint32_t byte = active ? byte_raw : 0;        // inactive lanes load a valid address
+  // source row m lives at (m < k ? dbase : cbase) + m*t  (checks: row k+i = check i)
+  const uint8_t *dbase = data + s * data_stride + byte;
+  const uint8_t *cbase = checks + s * checks_stride + byte - static_cast<uint64_t>(k) * t;
+  const uint32_t r0 = chunk * band_rows;              // first row of the chunk (relative)
+  const uint32_t rows = min(band_rows, nrows - r0);
+  // row_ptr[row_begin + r0 + i] for i = 0..rows in lanes 0..rows
+  const int32_t rp = lane <= rows ? __ldg(&row_ptr[row_begin + r0 + lane]) : 0;
+  const int32_t base = __shfl_sync(0xffffffffu, rp, 0);
+  const int32_t end = __shfl_sync(0xffffffffu, rp, rows);
+  uint8_t *out = coded + s * coded_stride + static_cast<uint64_t>(r0) * t + byte_raw;
+  uint32_t cur = 0;                                   // current row of the chunk
+  int32_t cur_end = __shfl_sync(0xffffffffu, rp, 1);  // its end edge
   uint4 acc = make_uint4(0, 0, 0, 0);
-  auto src = [&](int32_t m) -> const uint4 * {
-    return reinterpret_cast<const uint4 *>(static_cast<uint32_t>(m) < k
-                                               ? dsrc + static_cast<uint64_t>(m) * t
-                                               : csrc + static_cast<uint64_t>(m - k) * t);
-  };
-  for (; b + 4 <= end; b += 4) {
-    const int32_t m0 = __ldg(&col[b]), m1 = __ldg(&col[b + 1]), m2 = __ldg(&col[b + 2]), m3 = __ldg(&col[b + 3]);
-    const uint4 v0 = __ldg(src(m0)), v1 = __ldg(src(m1)), v2 = __ldg(src(m2)), v3 = __ldg(src(m3));
-    xor_into(acc, v0);
-    xor_into(acc, v1);
-    xor_into(acc, v2);
-    xor_into(acc, v3);
+  for (int32_t e0 = base; e0 < end; e0 += 32) {
+    // 32 column indices per coalesced load; positions past `end` read row 0 (never XORed)
+    const uint32_t cv = e0 + static_cast<int32_t>(lane) < end ? static_cast<uint32_t>(__ldg(&col[e0 + lane])) : 0u;
+    const int32_t nb = min(32, end - e0);
+    for (int32_t kk = 0; kk < nb; kk += kBandBatch) {
+      uint4 v[kBandBatch];
+#pragma unroll
+      for (uint32_t u = 0; u < kBandBatch; ++u) {
+        const uint32_t m = __shfl_sync(0xffffffffu, cv, kk + u);
+        const uint8_t *b0 = m < k ? dbase : cbase;
+        v[u] = __ldg(reinterpret_cast<const uint4 *>(b0 + static_cast<uint64_t>(m) * t));
+      }
+      const int32_t lim = min(static_cast<int32_t>(kBandBatch), nb - kk);
+#pragma unroll
+      for (int32_t u = 0; u < static_cast<int32_t>(kBandBatch); ++u) {
+        if (u >= lim) break;
+        if (e0 + kk + u == cur_end) {  // warp-uniform: the previous row is complete
+          if (active) st_stream(out + static_cast<uint64_t>(cur) * t, acc);
+          acc = make_uint4(0, 0, 0, 0);
+          ++cur;
+          cur_end = __shfl_sync(0xffffffffu, rp, cur + 1);
+        }
+        xor_into(acc, v[u]);
+      }
+    }
   }
-  for (; b < end; ++b) xor_into(acc, __ldg(src(__ldg(&col[b]))));
-  st_stream(coded + s * coded_stride + static_cast<uint64_t>(jr) * t + byte, acc);
+  if (active) st_stream(out + static_cast<uint64_t>(cur) * t, acc);  // the last row
 }
 
 // ===================================================================== host-side launch
@@ -527,14 +555,18 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
   }
   const uint32_t nrows = row_end - row_begin;
   if (nrows) {
-    const uint32_t nbands = (gslices + kBandSlices - 1) / kBandSlices;
-    const uint64_t items = static_cast<uint64_t>(S) * nbands * nrows * kBandSlices;
-    const uint64_t blocks = (items + kGroupsPerBlock - 1) / kGroupsPerBlock;
+    const uint32_t nbands = static_cast<uint32_t>((prm.t + kBandBytes - 1) / kBandBytes);
+    // rows per warp: up to kBandRowsMax, fewer if that leaves fewer than ~64 warps per SM
+    const uint64_t row_bands = static_cast<uint64_t>(S) * nbands * nrows;
+    const uint32_t band_rows = static_cast<uint32_t>(
+        std::max<uint64_t>(1, std::min<uint64_t>(kBandRowsMax, row_bands / (64ull * g.sm_count))));
+    const uint64_t units = static_cast<uint64_t>(S) * nbands * ((nrows + band_rows - 1) / band_rows);
+    const uint64_t blocks = (units + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
     if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
-    fsb_lt_global<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, prm.k, prm.t, gslices, nbands, row_begin, nrows, g.dev.lt_row_ptr, g.dev.lt_col, data, data_stride,
-        checks, checks_stride, coded, coded_stride);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_lt_global launch");
+    fsb_lt_band<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
+        S, prm.k, static_cast<uint32_t>(prm.t), nbands, row_begin, nrows, band_rows, g.dev.lt_row_ptr, g.dev.lt_col, data, data_stride, checks,
+        checks_stride, coded, coded_stride);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_lt_band launch");
     ++*launches;
   }
   return FS_OK;
