@@ -74,6 +74,7 @@ struct SmemSchedule {
 struct DeviceBufs {
   int device = -1;
   int32_t *pre_row_ptr = nullptr, *pre_col = nullptr, *lt_row_ptr = nullptr, *lt_col = nullptr;
+  uint32_t *lt_colf = nullptr;  // lt_col with bit 31 set on the last edge of each row
   uint32_t *sched = nullptr;
   uint32_t *warp_info = nullptr;
   uint16_t *pre_slots = nullptr;

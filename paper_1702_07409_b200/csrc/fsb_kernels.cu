@@ -341,7 +341,7 @@ constexpr uint32_t kBandBatch = 8;
 
 __global__ void __launch_bounds__(kGlobalThreads, 4)
     fsb_lt_band(uint32_t S, uint32_t k, uint32_t t, uint32_t nbands, uint32_t row_begin, uint32_t nrows,
-                uint32_t band_rows, const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                uint32_t band_rows, const int32_t *__restrict__ row_ptr, const uint32_t *__restrict__ colf,
                 const uint8_t *__restrict__ data, uint64_t data_stride, const uint8_t *__restrict__ checks,
                 uint64_t checks_stride, uint8_t *__restrict__ coded, uint64_t coded_stride) {
   const uint32_t lane = threadIdx.x & 31;
@@ -360,23 +360,22 @@ __global__ void __launch_bounds__(kGlobalThreads, 4)
   const uint8_t *cbase = checks + s * checks_stride + byte - static_cast<uint64_t>(k) * t;
   const uint32_t r0 = chunk * band_rows;              // first row of the chunk (relative)
   const uint32_t rows = min(band_rows, nrows - r0);
-  // row_ptr[row_begin + r0 + i] for i = 0..rows in lanes 0..rows
-  const int32_t rp = lane <= rows ? __ldg(&row_ptr[row_begin + r0 + lane]) : 0;
-  const int32_t base = __shfl_sync(0xffffffffu, rp, 0);
-  const int32_t end = __shfl_sync(0xffffffffu, rp, rows);
+  const int32_t base = __ldg(&row_ptr[row_begin + r0]);
+  const int32_t end = __ldg(&row_ptr[row_begin + r0 + rows]);
   uint8_t *out = coded + s * coded_stride + static_cast<uint64_t>(r0) * t + byte_raw;
-  uint32_t cur = 0;                                   // current row of the chunk
-  int32_t cur_end = __shfl_sync(0xffffffffu, rp, 1);  // its end edge
   uint4 acc = make_uint4(0, 0, 0, 0);
   for (int32_t e0 = base; e0 < end; e0 += 32) {
-    // 32 column indices per coalesced load; positions past `end` read row 0 (never XORed)
-    const uint32_t cv = e0 + static_cast<int32_t>(lane) < end ? static_cast<uint32_t>(__ldg(&col[e0 + lane])) : 0u;
+    // 32 marked column indices (bit 31 = last edge of its row) per coalesced load; positions
+    // past `end` read row 0 and are never XORed
+    const uint32_t cv = e0 + static_cast<int32_t>(lane) < end ? __ldg(&colf[e0 + lane]) : 0u;
     const int32_t nb = min(32, end - e0);
     for (int32_t kk = 0; kk < nb; kk += kBandBatch) {
       uint4 v[kBandBatch];
+      uint32_t mr[kBandBatch];
 #pragma unroll
       for (uint32_t u = 0; u < kBandBatch; ++u) {
-        const uint32_t m = __shfl_sync(0xffffffffu, cv, kk + u);
+        mr[u] = __shfl_sync(0xffffffffu, cv, kk + u);
+        const uint32_t m = mr[u] & 0x7FFFFFFFu;
         const uint8_t *b0 = m < k ? dbase : cbase;
         v[u] = __ldg(reinterpret_cast<const uint4 *>(b0 + static_cast<uint64_t>(m) * t));
       }
@@ -384,17 +383,15 @@ __global__ void __launch_bounds__(kGlobalThreads, 4)
 #pragma unroll
       for (int32_t u = 0; u < static_cast<int32_t>(kBandBatch); ++u) {
         if (u >= lim) break;
-        if (e0 + kk + u == cur_end) {  // warp-uniform: the previous row is complete
-          if (active) st_stream(out + static_cast<uint64_t>(cur) * t, acc);
-          acc = make_uint4(0, 0, 0, 0);
-          ++cur;
-          cur_end = __shfl_sync(0xffffffffu, rp, cur + 1);
-        }
         xor_into(acc, v[u]);
+        if (mr[u] >> 31) {  // warp-uniform: the row is complete
+          if (active) st_stream(out, acc);
+          acc = make_uint4(0, 0, 0, 0);
+          out += t;
+        }
       }
     }
   }
-  if (active) st_stream(out + static_cast<uint64_t>(cur) * t, acc);  // the last row
 }
 
 // ===================================================================== host-side launch
@@ -445,6 +442,7 @@ void free_device(Graph &g) {
   cudaFree(d.pre_col);
   cudaFree(d.lt_row_ptr);
   cudaFree(d.lt_col);
+  cudaFree(d.lt_colf);
   cudaFree(d.sched);
   cudaFree(d.warp_info);
   cudaFree(d.pre_slots);
@@ -466,6 +464,11 @@ fs_status upload_graph(Graph &g) {
   if ((st = upload(&g.dev.pre_col, g.pre_col.data(), g.pre_col.size())) != FS_OK) return st;
   if ((st = upload(&g.dev.lt_row_ptr, g.lt_row_ptr.data(), g.lt_row_ptr.size())) != FS_OK) return st;
   if ((st = upload(&g.dev.lt_col, g.lt_col.data(), g.lt_col.size())) != FS_OK) return st;
+  {  // column indices marked with the last edge of each row (bit 31), for fsb_lt_band
+    std::vector<uint32_t> colf(g.lt_col.begin(), g.lt_col.end());
+    for (uint32_t j = 0; j < g.prm.n; ++j) colf[g.lt_row_ptr[j + 1] - 1] |= 0x80000000u;
+    if ((st = upload(&g.dev.lt_colf, colf.data(), colf.size())) != FS_OK) return st;
+  }
   if (g.smem_eligible) {
     // two tile buffers + the schedule + 6 mbarriers
     const uint64_t bytes = 2ull * g.sched.tile_units * kUnitBytes + g.sched.words.size() * 4 + 6 * 8;
@@ -564,7 +567,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     const uint64_t blocks = (units + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
     if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
     fsb_lt_band<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, prm.k, static_cast<uint32_t>(prm.t), nbands, row_begin, nrows, band_rows, g.dev.lt_row_ptr, g.dev.lt_col, data, data_stride, checks,
+        S, prm.k, static_cast<uint32_t>(prm.t), nbands, row_begin, nrows, band_rows, g.dev.lt_row_ptr, g.dev.lt_colf, data, data_stride, checks,
         checks_stride, coded, coded_stride);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_lt_band launch");
     ++*launches;
