@@ -337,9 +337,9 @@ __global__ void __launch_bounds__(kGlobalThreads)
 // source about once, the gathers hit L2.
 constexpr uint32_t kBandBytes = 512;
 constexpr uint32_t kBandRowsMax = 8;   // coded rows per warp (fewer when the call is small)
-constexpr uint32_t kBandBatch = 8;
+constexpr uint32_t kBandBatch = 4;
 
-__global__ void __launch_bounds__(kGlobalThreads, 4)
+__global__ void __launch_bounds__(kGlobalThreads, 6)
     fsb_lt_band(uint32_t S, uint32_t k, uint32_t t, uint32_t nbands, uint32_t row_begin, uint32_t nrows,
                 uint32_t band_rows, const int32_t *__restrict__ row_ptr, const uint32_t *__restrict__ colf,
                 const uint8_t *__restrict__ data, uint64_t data_stride, const uint8_t *__restrict__ checks,
