@@ -166,6 +166,11 @@ FSB_API fs_status fs_graph_schedule(const fs_graph *g, const uint32_t **words, u
                                     uint32_t *cont_base, const uint32_t **warp_info, uint32_t *nwarps,
                                     uint32_t *kpad, uint32_t *zero_even);
 
+/* Profiling aid (only meaningful when the process runs with FSB_DEBUG=2): copies out and clears
+ * n <= 64 counters of the SMEM kernel: for consumer warp w, [2w] = cycles spent waiting for tiles,
+ * [2w+1] = total cycles, each summed over all CTAs since the last call.                    */
+FSB_API fs_status fs_debug_counters(uint64_t *out, uint32_t n);
+
 /* Number of kernel launches the last successful fs_encode / fs_encode_stripes on this
  * thread enqueued (for launch accounting in benchmarks).                                 */
 FSB_API uint32_t fs_last_launch_count(void);

@@ -232,6 +232,11 @@ fs_status fs_graph_schedule(const fs_graph *h, const uint32_t **words, uint64_t 
   return FS_OK;
 }
 
+fs_status fs_debug_counters(uint64_t *out, uint32_t n) {
+  if (!out) { set_error("null argument"); return FS_EINVAL; }
+  return fsb::read_debug_counters(out, n);
+}
+
 uint32_t fs_last_launch_count(void) { return fsb::g_launches; }
 
 void fs_free(fs_graph *h) {

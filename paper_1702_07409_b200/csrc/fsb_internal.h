@@ -110,6 +110,8 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
                         uint64_t coded_stride, uint32_t row_begin, uint32_t row_end, void *stream,
                         uint32_t *launches);
 
+fs_status read_debug_counters(uint64_t *out, uint32_t n);
+
 // fsb_capi.cpp
 void set_error(const std::string &msg);
 

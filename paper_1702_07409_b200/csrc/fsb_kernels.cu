@@ -63,6 +63,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// Wait with a fixed sleep between probes, for warps that are early and have nothing else to do:
+// each probe reads the barrier through the shared-memory pipe, so fast polling (or a suspend that
+// wakes on every barrier event in the CTA) steals pipe cycles from the warps still computing.
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity, uint32_t ns) {
+  for (;;) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+  }
+}
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int32_t c0,
                                             int32_t c1, int32_t c2) {
   asm volatile(
@@ -88,6 +104,9 @@ __device__ __forceinline__ void st_stream(uint8_t *p, const uint4 &v) {
 }
 
 // ============================================================================ SMEM kernel
+// Profiling experiments only (FSB_DEBUG=2): per consumer warp, cycles spent waiting for a tile
+// (ready/full barriers) and total cycles, summed over CTAs (read with fs_debug_counters).
+__device__ unsigned long long g_debug_counters[2 * 32];
 struct SmemArgs {
   const uint4 *sched;          // heads ++ conts chunk streams (fsb_internal.h: SmemSchedule)
   const uint32_t *warp_info;   // kConsumerWarps x {items, head_off, cont_off}
@@ -99,6 +118,8 @@ struct SmemArgs {
   uint64_t t;
   uint32_t nslices, ntiles, p, d_p, kpad, zero_even, data_units, tile_units;
   uint32_t sched_chunks, cont_base;
+  uint32_t debug;              // FSB_DEBUG bits (profiling experiments only; 0 in production)
+  uint32_t wait_ns;            // consumer sleep between probes of a tile's `ready` barrier
 };
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -276,14 +297,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t cont0 =
       smem_u32(sched_s) + (a.cont_base + __ldg(&a.warp_info[warp * 3 + 2])) * kChunkBytes + half_id * 16;
   uint32_t i = 0;
+  const long long t_start = (a.debug & 2) ? clock64() : 0;
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
     const uint32_t b = i & 1, ph = (i >> 1) & 1;
     const uint32_t stripe = tile / a.nslices, slice = tile % a.nslices;
     const uint32_t sbase = smem_base + b * buf_bytes + lane4 * 16;  // this lane's 16 B of tile row 0
     uint32_t hp = head0, cp = cont0;
     uint4 h0 = lds128(hp);
-    mbar_wait(smem_u32(&ready[b]), ph);
+    long long t_wait0 = 0;
+    if (a.debug & 2) t_wait0 = clock64();
+    mbar_wait_backoff(smem_u32(&ready[b]), ph, a.wait_ns);
     mbar_wait(smem_u32(&full[b]), ph);
+    if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2], static_cast<unsigned long long>(clock64() - t_wait0));
     uint8_t *out = a.coded + stripe * a.coded_stride + static_cast<uint64_t>(slice) * kSliceBytes + lane4 * 16;
     // items, with the next head chunk in flight (2-way unrolled so no register moves)
     for (uint32_t it = 0; it < nitems; it += 2) {
@@ -297,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[b]));
   }
+  if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2 + 1], static_cast<unsigned long long>(clock64() - t_start));
 }
 
 // ========================================================================= GLOBAL kernels
@@ -541,6 +567,18 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     a.tile_units = g.sched.tile_units;
     a.sched_chunks = static_cast<uint32_t>(g.sched.words.size() / (kChunkBytes / 4));
     a.cont_base = g.sched.cont_base;
+    {
+      static const uint32_t dbg = [] {
+        const char *e = std::getenv("FSB_DEBUG");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+      }();
+      a.debug = dbg;
+      static const uint32_t wns = [] {
+        const char *e = std::getenv("FSB_WAIT_NS");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 500u;
+      }();
+      a.wait_ns = wns;
+    }
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, g.sm_count));
     fsb_smem_encode<<<grid, kThreads, g.smem_bytes, stream>>>(tmap, a);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_smem_encode launch");
@@ -572,6 +610,17 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_lt_band launch");
     ++*launches;
   }
+  return FS_OK;
+}
+
+fs_status read_debug_counters(uint64_t *out, uint32_t n) {
+  unsigned long long buf[64] = {0};
+  cudaError_t e = cudaMemcpyFromSymbol(buf, g_debug_counters, sizeof(buf));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyFromSymbol");
+  for (uint32_t i = 0; i < n && i < 64; ++i) out[i] = buf[i];
+  const unsigned long long zero[64] = {0};
+  e = cudaMemcpyToSymbol(g_debug_counters, zero, sizeof(zero));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
   return FS_OK;
 }
 

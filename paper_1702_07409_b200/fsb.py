@@ -20,7 +20,7 @@ VARIANT_AUTO, VARIANT_SMEM, VARIANT_GLOBAL = 0, 1, 2
 # Every symbol include/fsb.h declares (checked by tests/test_capi.py).
 EXPORTS = ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get_info",
            "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_last_launch_count",
-           "fs_free", "fs_last_error", "fs_version", "fs_graph_schedule")
+           "fs_free", "fs_last_error", "fs_version", "fs_graph_schedule", "fs_debug_counters")
 
 
 class FsError(RuntimeError):
@@ -72,6 +72,8 @@ def lib():
         for f in ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get_info",
                   "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_graph_schedule"):
             getattr(L, f).restype = ctypes.c_int
+        L.fs_debug_counters.argtypes = [P, u32]
+        L.fs_debug_counters.restype = ctypes.c_int
         L.fs_last_launch_count.restype = u32
         L.fs_last_launch_count.argtypes = []
         L.fs_free.argtypes = [P]
@@ -226,6 +228,13 @@ class Graph:
             self.free()
         except Exception:
             pass
+
+
+def debug_counters(n=64):
+    """fs_debug_counters (profiling aid, FSB_DEBUG=2): uint64 counters, cleared on read."""
+    out = (ctypes.c_uint64 * n)()
+    _check(lib().fs_debug_counters(ctypes.cast(out, ctypes.c_void_p), n))
+    return [int(x) for x in out]
 
 
 def version():
