@@ -363,9 +363,9 @@ __global__ void __launch_bounds__(kGlobalThreads)
 // source about once, the gathers hit L2.
 constexpr uint32_t kBandBytes = 512;
 constexpr uint32_t kBandRowsMax = 8;   // coded rows per warp (fewer when the call is small)
-constexpr uint32_t kBandBatch = 4;
 
-__global__ void __launch_bounds__(kGlobalThreads, 6)
+template <uint32_t kBandBatch, int kMinBlocks>
+__global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
     fsb_lt_band(uint32_t S, uint32_t k, uint32_t t, uint32_t nbands, uint32_t row_begin, uint32_t nrows,
                 uint32_t band_rows, const int32_t *__restrict__ row_ptr, const uint32_t *__restrict__ colf,
                 const uint8_t *__restrict__ data, uint64_t data_stride, const uint8_t *__restrict__ checks,
@@ -604,9 +604,19 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     const uint64_t units = static_cast<uint64_t>(S) * nbands * ((nrows + band_rows - 1) / band_rows);
     const uint64_t blocks = (units + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
     if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
-    fsb_lt_band<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, prm.k, static_cast<uint32_t>(prm.t), nbands, row_begin, nrows, band_rows, g.dev.lt_row_ptr, g.dev.lt_colf, data, data_stride, checks,
-        checks_stride, coded, coded_stride);
+    // (gathers in flight per warp, blocks per SM); measured on config 5 (tools/gpu/sweep_band.sh):
+    // (2, 8) 0.281 ms, (4, 6) 0.292, (8, 4) 0.299, (8, 5) 0.371 (spills), (4, 8) 0.381 (spills).
+    // Tuning knob FSB_BAND_CFG selects another instance.
+    static const int band_cfg = [] {
+      const char *e = std::getenv("FSB_BAND_CFG");
+      return e ? std::atoi(e) : 4;
+    }();
+    auto kern = fsb_lt_band<2, 8>;
+    if (band_cfg == 0) kern = fsb_lt_band<4, 6>;
+    if (band_cfg == 2) kern = fsb_lt_band<8, 4>;
+    kern<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
+        S, prm.k, static_cast<uint32_t>(prm.t), nbands, row_begin, nrows, band_rows, g.dev.lt_row_ptr,
+        g.dev.lt_colf, data, data_stride, checks, checks_stride, coded, coded_stride);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_lt_band launch");
     ++*launches;
   }
