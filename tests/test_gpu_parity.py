@@ -237,3 +237,38 @@ def test_decode_gpu_output_roundtrip():
     ok = state[:cfg["k"]] != 0
     assert ok.sum() > 0.9 * cfg["k"]
     assert np.array_equal(I[:cfg["k"]][ok], D[ok])
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_parameters(seed):
+    """Random (k, p, d_p, n, t, distribution, stripes): every variant bit-exact vs the oracle
+    (covers ragged t, k not a multiple of the TMA box, heavy rows, pair and warp splits)."""
+    _need_gpu()
+    rng = np.random.default_rng(1000 + seed)
+    k = int(rng.integers(1, 1500))
+    p = int(rng.integers(0, 60))
+    d_p = int(rng.integers(1, min(k, 6) + 1)) if p else 0
+    n = int(rng.integers(1, 2200))
+    t = int(rng.choice([16, 48, 64, 128, 192, 512, 1088, 4096]))
+    if rng.random() < 0.5:
+        cfg = dict(k=k, p=p, d_p=d_p, n=n, t=t, dist=configs.RSD, rsd_c=float(rng.uniform(0.03, 0.3)),
+                   rsd_delta=float(rng.uniform(0.01, 0.5)), seed=int(rng.integers(1, 1 << 40)))
+    else:
+        cfg = dict(k=k, p=p, d_p=d_p, n=n, t=t, dist=configs.FINITE, seed=int(rng.integers(1, 1 << 40)),
+                   fin_deg=configs.OMEGA_DEGREES, fin_prob=configs.OMEGA_PROBS)
+    S = int(rng.choice([1, 3, 150, 400])) if k * t <= (1 << 20) else 1
+    cfg["stripes"] = S
+    try:
+        go = oracle.generate_graph(cfg)
+    except ValueError:
+        pytest.skip("parameters rejected by the distribution rules (e.g. RSD spike K/R < 1)")
+    D = inputs.stripe_data(cfg).numpy()
+    C, Y = oracle.encode(go, D)
+    variants = [fsb.VARIANT_AUTO, fsb.VARIANT_GLOBAL]
+    if fsb.Graph.create(cfg).info()["smem_eligible"]:
+        variants.append(fsb.VARIANT_SMEM)
+    for v in variants:
+        _, c, y = _run(cfg, v, data=torch.from_numpy(D).cuda())
+        if p:
+            _assert_equal(c, C, "seed %d checks v%d" % (seed, v))
+        _assert_equal(y, Y, "seed %d coded v%d" % (seed, v))
