@@ -166,6 +166,47 @@ FSB_API fs_status fs_graph_schedule(const fs_graph *g, const uint32_t **words, u
                                     uint32_t *cont_base, const uint32_t **warp_info, uint32_t *nwarps,
                                     uint32_t *kpad, uint32_t *zero_even);
 
+/* ---------------------------------------------------------------- decoder
+ * Decoding is split like the encoder: a graph-only plan on the host, then data-parallel XOR on
+ * the GPU.  The plan follows Alg 5 (DPG): equations are the received LT rows
+ * (Y_j = XOR of its neighbours) and the p precode checks (0 = XOR of P(i) and C_i; "BP at most
+ * twice"); at level L every equation with exactly one unknown left recovers it, one
+ * equation per unknown -- the lowest-degree one (ties: lowest index, LT rows
+ * before checks) -- so a level's rows are independent.  The recovered set is the
+ * peeling closure of Alg 1; unknowns in a stopping set stay unrecovered (the
+ * paper's BP returns them as F).                                                             */
+typedef struct fs_decode_plan fs_decode_plan;  /* opaque, immutable after creation */
+
+typedef struct {
+  uint32_t K;                /* intermediate symbols k+p                                        */
+  uint32_t n;                /* coded symbols                                                   */
+  uint32_t received;         /* received coded symbols                                          */
+  uint32_t recovered;        /* intermediate symbols the plan recovers                          */
+  uint32_t recovered_data;   /* ... of them data symbols (index < k)                            */
+  uint32_t levels;           /* DPG levels (GPU launches per fs_decode)                         */
+  uint32_t rows;             /* rows of the plan (= recovered)                                  */
+  uint32_t max_level_rows;   /* largest level                                                   */
+  uint64_t xor_sources;      /* total sources over all rows (XOR work per byte column)          */
+} fs_decode_info;
+
+/* Build the plan for graph g and the received set: received[j] != 0 iff coded symbol j is
+ * available (n bytes, host).  flags: FS_GRAPH_HOST_ONLY = no device copy (fs_decode then
+ * returns FS_EUNSUPPORTED).  FS_EINVAL on NULL arguments.                                   */
+FSB_API fs_status fs_decode_plan_create(const fs_graph *g, const uint8_t *received, uint32_t flags,
+                                        fs_decode_plan **out);
+FSB_API fs_status fs_decode_plan_info(const fs_decode_plan *plan, fs_decode_info *info);
+/* Host views owned by the plan: state[K] (1 = recovered), level_of[K] (level, -1). */
+FSB_API fs_status fs_decode_plan_state(const fs_decode_plan *plan, const uint8_t **state,
+                                       const int32_t **level_of);
+/* Run the plan on num_stripes stripes: d_coded = coded symbols (row j at d_coded + s*coded_stride
+ * + j*t; rows not received are never read), d_inter = output intermediate symbols (row m at
+ * d_inter + s*inter_stride + m*t; rows the plan recovers are written, the others untouched;
+ * data symbols are rows 0..k-1).  Strides multiples of 16 and >= n*t, (k+p)*t.  One launch per
+ * level on `stream`.                                                                          */
+FSB_API fs_status fs_decode(const fs_decode_plan *plan, uint32_t num_stripes, const uint8_t *d_coded,
+                            uint64_t coded_stride, uint8_t *d_inter, uint64_t inter_stride, void *stream);
+FSB_API void fs_decode_plan_free(fs_decode_plan *plan);  /* NULL-safe */
+
 /* Profiling aid (only meaningful when the process runs with FSB_DEBUG=2): copies out and clears
  * n <= 64 counters of the SMEM kernel: for consumer warp w, [2w] = cycles spent waiting for tiles,
  * [2w+1] = total cycles, each summed over all CTAs since the last call.                    */

@@ -237,6 +237,83 @@ fs_status fs_debug_counters(uint64_t *out, uint32_t n) {
   return fsb::read_debug_counters(out, n);
 }
 
+fs_status fs_decode_plan_create(const fs_graph *h, const uint8_t *received, uint32_t flags, fs_decode_plan **out) {
+  fsb::set_error("");
+  if (!h || !received || !out) { set_error("null argument"); return FS_EINVAL; }
+  *out = nullptr;
+  fs_decode_plan *d = new (std::nothrow) fs_decode_plan();
+  if (!d) { set_error("out of host memory"); return FS_ENOMEM; }
+  fs_status st;
+  try {
+    st = fsb::build_decode_plan(h->g, received, d->pl);
+  } catch (const std::bad_alloc &) {
+    st = FS_ENOMEM;
+    set_error("out of host memory");
+  }
+  if (st == FS_OK && !(flags & FS_GRAPH_HOST_ONLY)) st = fsb::upload_decode_plan(d->pl);
+  if (st != FS_OK) {
+    fsb::free_decode_plan(d->pl);
+    delete d;
+    return st;
+  }
+  *out = d;
+  return FS_OK;
+}
+
+fs_status fs_decode_plan_info(const fs_decode_plan *d, fs_decode_info *info) {
+  if (!d || !info) { set_error("null argument"); return FS_EINVAL; }
+  const fsb::DecodePlan &pl = d->pl;
+  std::memset(info, 0, sizeof(*info));
+  info->K = pl.K;
+  info->n = pl.n;
+  info->received = pl.received;
+  info->levels = static_cast<uint32_t>(pl.level_ptr.size() - 1);
+  info->rows = static_cast<uint32_t>(pl.target.size());
+  for (uint32_t m = 0; m < pl.K; ++m) {
+    info->recovered += pl.state[m];
+    if (m < pl.k) info->recovered_data += pl.state[m];
+  }
+  for (size_t L = 0; L + 1 < pl.level_ptr.size(); ++L)
+    info->max_level_rows = std::max<uint32_t>(info->max_level_rows, pl.level_ptr[L + 1] - pl.level_ptr[L]);
+  info->xor_sources = pl.src.size();
+  return FS_OK;
+}
+
+fs_status fs_decode_plan_state(const fs_decode_plan *d, const uint8_t **state, const int32_t **level_of) {
+  if (!d) { set_error("null argument"); return FS_EINVAL; }
+  if (state) *state = d->pl.state.data();
+  if (level_of) *level_of = d->pl.level_of.data();
+  return FS_OK;
+}
+
+fs_status fs_decode(const fs_decode_plan *d, uint32_t S, const uint8_t *d_coded, uint64_t coded_stride,
+                    uint8_t *d_inter, uint64_t inter_stride, void *stream) {
+  fsb::set_error("");
+  fsb::g_launches = 0;
+  if (!d) { set_error("null plan"); return FS_EINVAL; }
+  const fsb::DecodePlan &pl = d->pl;
+  if (pl.device < 0) { set_error("host-only plan has no device copy"); return FS_EUNSUPPORTED; }
+  if (S == 0) return FS_OK;
+  if (!d_coded || !aligned16(d_coded) || coded_stride < pl.n * pl.t || coded_stride % 16) {
+    set_error("d_coded must be 16-B aligned with coded_stride >= n*t, a multiple of 16");
+    return FS_EINVAL;
+  }
+  if (!d_inter || !aligned16(d_inter) || inter_stride < static_cast<uint64_t>(pl.K) * pl.t || inter_stride % 16) {
+    set_error("d_inter must be 16-B aligned with inter_stride >= (k+p)*t, a multiple of 16");
+    return FS_EINVAL;
+  }
+  uint32_t launches = 0;
+  fs_status st = fsb::launch_decode(pl, S, d_coded, coded_stride, d_inter, inter_stride, stream, &launches);
+  if (st == FS_OK) fsb::g_launches = launches;
+  return st;
+}
+
+void fs_decode_plan_free(fs_decode_plan *d) {
+  if (!d) return;
+  fsb::free_decode_plan(d->pl);
+  delete d;
+}
+
 uint32_t fs_last_launch_count(void) { return fsb::g_launches; }
 
 void fs_free(fs_graph *h) {

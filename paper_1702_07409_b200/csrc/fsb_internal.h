@@ -120,3 +120,37 @@ void set_error(const std::string &msg);
 struct fs_graph {
   fsb::Graph g;
 };
+
+// ------------------------------------------------------------------ decoder (NEXT-1, Alg 5)
+namespace fsb {
+// Decoding path of one (graph, received set): Alg 5 (DPG) levels over the received LT rows and
+// the precode checks.  Row r of the plan recovers intermediate symbol target[r] as the XOR of
+// its sources src[src_ptr[r] .. src_ptr[r+1]): an intermediate index m (recovered at an earlier
+// level) or m | kSrcCoded for received coded row m; bit 31 (kSrcLast) marks a row's last source.
+constexpr uint32_t kSrcCoded = 1u << 30;
+constexpr uint32_t kSrcLast = 1u << 31;
+struct DecodePlan {
+  uint32_t k = 0, p = 0, n = 0, K = 0;
+  uint64_t t = 0;
+  uint32_t received = 0;
+  std::vector<uint32_t> level_ptr;   // levels+1 row offsets
+  std::vector<int32_t> target;       // rows
+  std::vector<int32_t> src_ptr;      // rows+1
+  std::vector<uint32_t> src;         // flagged source list
+  std::vector<uint8_t> state;        // K: 1 recovered, 0 not
+  std::vector<int32_t> level_of;     // K: level that recovered it, -1
+  int device = -1;
+  int32_t *d_target = nullptr, *d_src_ptr = nullptr;
+  uint32_t *d_src = nullptr;
+  int sm_count = 0;
+};
+fs_status build_decode_plan(const Graph &g, const uint8_t *received, DecodePlan &pl);
+fs_status upload_decode_plan(DecodePlan &pl);
+void free_decode_plan(DecodePlan &pl);
+fs_status launch_decode(const DecodePlan &pl, uint32_t S, const uint8_t *coded, uint64_t coded_stride,
+                        uint8_t *inter, uint64_t inter_stride, void *stream, uint32_t *launches);
+}  // namespace fsb
+
+struct fs_decode_plan {
+  fsb::DecodePlan pl;
+};

@@ -420,6 +420,67 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   }
 }
 
+// ====================================================================== decoder (NEXT-1)
+// One DPG level (fsb_decode.cpp): row r recovers intermediate symbol target[r] of every stripe as
+// the XOR of its sources (intermediate rows recovered at earlier levels, or a received coded
+// row).  Same layout and schedule as fsb_lt_band: one warp per (stripe, 512-B band, chunk of
+// rows), source indices 32 per coalesced load, bit 31 = a row's last source.
+template <uint32_t kBatch, int kMinBlocks>
+__global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
+    fsb_dpg_level(uint32_t S, uint32_t t, uint32_t nbands, uint32_t row0, uint32_t nrows, uint32_t band_rows,
+                  const int32_t *__restrict__ target, const int32_t *__restrict__ src_ptr,
+                  const uint32_t *__restrict__ src, const uint8_t *__restrict__ coded, uint64_t coded_stride,
+                  uint8_t *inter, uint64_t inter_stride) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nchunks = (nrows + band_rows - 1) / band_rows;
+  uint64_t unit = static_cast<uint64_t>(blockIdx.x) * (kGlobalThreads / 32) + (threadIdx.x >> 5);
+  const uint32_t chunk = static_cast<uint32_t>(unit % nchunks);
+  unit /= nchunks;
+  const uint32_t band = static_cast<uint32_t>(unit % nbands);
+  const uint64_t s = unit / nbands;
+  if (s >= S) return;
+  const uint32_t byte_raw = band * kBandBytes + lane * 16;
+  const bool active = byte_raw < t;
+  const uint32_t byte = active ? byte_raw : 0;
+  const uint8_t *ibase = inter + s * inter_stride + byte;  // read: rows of earlier levels
+  const uint8_t *cbase = coded + s * coded_stride + byte;
+  uint8_t *obase = inter + s * inter_stride + byte_raw;
+  const uint32_t r0 = row0 + chunk * band_rows;
+  const uint32_t rows = min(band_rows, row0 + nrows - r0);
+  const int32_t tg = lane < rows ? __ldg(&target[r0 + lane]) : 0;
+  const int32_t base = __ldg(&src_ptr[r0]);
+  const int32_t end = __ldg(&src_ptr[r0 + rows]);
+  uint32_t cur = 0;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  for (int32_t e0 = base; e0 < end; e0 += 32) {
+    const uint32_t cv = e0 + static_cast<int32_t>(lane) < end ? __ldg(&src[e0 + lane]) : 0u;
+    const int32_t nb = min(32, end - e0);
+    for (int32_t kk = 0; kk < nb; kk += kBatch) {
+      uint4 v[kBatch];
+      uint32_t fl[kBatch];
+#pragma unroll
+      for (uint32_t u = 0; u < kBatch; ++u) {
+        fl[u] = __shfl_sync(0xffffffffu, cv, kk + u);
+        const uint32_t m = fl[u] & (kSrcCoded - 1);
+        const uint8_t *b0 = (fl[u] & kSrcCoded) ? cbase : ibase;
+        v[u] = __ldg(reinterpret_cast<const uint4 *>(b0 + static_cast<uint64_t>(m) * t));
+      }
+      const int32_t lim = min(static_cast<int32_t>(kBatch), nb - kk);
+#pragma unroll
+      for (int32_t u = 0; u < static_cast<int32_t>(kBatch); ++u) {
+        if (u >= lim) break;
+        xor_into(acc, v[u]);
+        if (fl[u] & kSrcLast) {  // warp-uniform: row complete
+          const uint32_t f = static_cast<uint32_t>(__shfl_sync(0xffffffffu, tg, cur));
+          if (active) *reinterpret_cast<uint4 *>(obase + static_cast<uint64_t>(f) * t) = acc;
+          acc = make_uint4(0, 0, 0, 0);
+          ++cur;
+        }
+      }
+    }
+  }
+}
+
 // ===================================================================== host-side launch
 namespace {
 
@@ -618,6 +679,58 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
         S, prm.k, static_cast<uint32_t>(prm.t), nbands, row_begin, nrows, band_rows, g.dev.lt_row_ptr,
         g.dev.lt_colf, data, data_stride, checks, checks_stride, coded, coded_stride);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_lt_band launch");
+    ++*launches;
+  }
+  return FS_OK;
+}
+
+fs_status upload_decode_plan(DecodePlan &pl) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  pl.device = dev;
+  if ((e = cudaDeviceGetAttribute(&pl.sm_count, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+    return cuda_fail(e, "cudaDeviceGetAttribute");
+  fs_status st;
+  if ((st = upload(&pl.d_target, pl.target.data(), pl.target.size())) != FS_OK) return st;
+  if ((st = upload(&pl.d_src_ptr, pl.src_ptr.data(), pl.src_ptr.size())) != FS_OK) return st;
+  if ((st = upload(&pl.d_src, pl.src.data(), pl.src.size())) != FS_OK) return st;
+  return FS_OK;
+}
+
+void free_decode_plan(DecodePlan &pl) {
+  if (pl.device < 0) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(pl.device);
+  cudaFree(pl.d_target);
+  cudaFree(pl.d_src_ptr);
+  cudaFree(pl.d_src);
+  if (prev >= 0) cudaSetDevice(prev);
+  pl.d_target = pl.d_src_ptr = nullptr;
+  pl.d_src = nullptr;
+  pl.device = -1;
+}
+
+fs_status launch_decode(const DecodePlan &pl, uint32_t S, const uint8_t *coded, uint64_t coded_stride,
+                        uint8_t *inter, uint64_t inter_stride, void *stream_ptr, uint32_t *launches) {
+  *launches = 0;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  const uint32_t nbands = static_cast<uint32_t>((pl.t + kBandBytes - 1) / kBandBytes);
+  for (size_t L = 0; L + 1 < pl.level_ptr.size(); ++L) {
+    const uint32_t row0 = pl.level_ptr[L], nrows = pl.level_ptr[L + 1] - row0;
+    if (!nrows) continue;
+    const uint64_t row_bands = static_cast<uint64_t>(S) * nbands * nrows;
+    const uint32_t band_rows = static_cast<uint32_t>(
+        std::max<uint64_t>(1, std::min<uint64_t>(kBandRowsMax, row_bands / (64ull * pl.sm_count))));
+    const uint64_t units = static_cast<uint64_t>(S) * nbands * ((nrows + band_rows - 1) / band_rows);
+    const uint64_t blocks = (units + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
+    if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
+    fsb_dpg_level<2, 6><<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
+        S, static_cast<uint32_t>(pl.t), nbands, row0, nrows, band_rows, pl.d_target, pl.d_src_ptr, pl.d_src, coded,
+        coded_stride, inter, inter_stride);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "fsb_dpg_level launch");
     ++*launches;
   }
   return FS_OK;

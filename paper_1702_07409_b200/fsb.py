@@ -20,7 +20,9 @@ VARIANT_AUTO, VARIANT_SMEM, VARIANT_GLOBAL = 0, 1, 2
 # Every symbol include/fsb.h declares (checked by tests/test_capi.py).
 EXPORTS = ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get_info",
            "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_last_launch_count",
-           "fs_free", "fs_last_error", "fs_version", "fs_graph_schedule", "fs_debug_counters")
+           "fs_free", "fs_last_error", "fs_version", "fs_graph_schedule", "fs_debug_counters",
+           "fs_decode_plan_create", "fs_decode_plan_info", "fs_decode_plan_state", "fs_decode",
+           "fs_decode_plan_free")
 
 
 class FsError(RuntimeError):
@@ -48,6 +50,13 @@ class fs_graph_info(ctypes.Structure):
                 ("device", ctypes.c_int32)]
 
 
+class fs_decode_info(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_uint32), ("n", ctypes.c_uint32), ("received", ctypes.c_uint32),
+                ("recovered", ctypes.c_uint32), ("recovered_data", ctypes.c_uint32),
+                ("levels", ctypes.c_uint32), ("rows", ctypes.c_uint32),
+                ("max_level_rows", ctypes.c_uint32), ("xor_sources", ctypes.c_uint64)]
+
+
 _lib = None
 
 
@@ -72,6 +81,14 @@ def lib():
         for f in ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get_info",
                   "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_graph_schedule"):
             getattr(L, f).restype = ctypes.c_int
+        L.fs_decode_plan_create.argtypes = [P, P, u32, PP]
+        L.fs_decode_plan_info.argtypes = [P, ctypes.POINTER(fs_decode_info)]
+        L.fs_decode_plan_state.argtypes = [P, PP, PP]
+        L.fs_decode.argtypes = [P, u32, P, u64, P, u64, P]
+        for f in ("fs_decode_plan_create", "fs_decode_plan_info", "fs_decode_plan_state", "fs_decode"):
+            getattr(L, f).restype = ctypes.c_int
+        L.fs_decode_plan_free.argtypes = [P]
+        L.fs_decode_plan_free.restype = None
         L.fs_debug_counters.argtypes = [P, u32]
         L.fs_debug_counters.restype = ctypes.c_int
         L.fs_last_launch_count.restype = u32
@@ -221,6 +238,53 @@ class Graph:
     def free(self):
         if self._h:
             lib().fs_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class DecodePlan:
+    """Owner of an fs_decode_plan: Alg 5 (DPG) levels for a graph and a received set."""
+
+    def __init__(self, graph, received, host_only=False):
+        rv = np.ascontiguousarray(np.asarray(received, dtype=bool).astype(np.uint8))
+        if rv.shape != (graph.n,):
+            raise ValueError("received must have n entries")
+        self.graph = graph
+        self._h = None
+        h = ctypes.c_void_p()
+        _check(lib().fs_decode_plan_create(graph._h, rv.ctypes.data_as(ctypes.c_void_p),
+                                           FS_GRAPH_HOST_ONLY if host_only else 0, ctypes.byref(h)))
+        self._h = h
+
+    def info(self):
+        inf = fs_decode_info()
+        _check(lib().fs_decode_plan_info(self._h, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in fs_decode_info._fields_}
+
+    def state(self):
+        """(state uint8[K], level_of int32[K]) copies."""
+        s, lv = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().fs_decode_plan_state(self._h, ctypes.byref(s), ctypes.byref(lv)))
+        K = self.graph.K
+        st = np.ctypeslib.as_array(ctypes.cast(s, ctypes.POINTER(ctypes.c_uint8)), (K,)).copy()
+        lev = np.ctypeslib.as_array(ctypes.cast(lv, ctypes.POINTER(ctypes.c_int32)), (K,)).copy()
+        return st, lev
+
+    def decode(self, coded, inter, stream=None):
+        """fs_decode over contiguous [S,n,t] coded and [S,K,t] intermediate uint8 CUDA tensors."""
+        S = coded.shape[0]
+        t = self.graph.t
+        _check(lib().fs_decode(self._h, S, _ptr(coded), self.graph.n * t, _ptr(inter), self.graph.K * t,
+                               _stream(stream)))
+
+    def free(self):
+        if self._h:
+            lib().fs_decode_plan_free(self._h)
             self._h = None
 
     def __del__(self):
