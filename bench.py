@@ -195,9 +195,21 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--op", default="encode", choices=["encode", "decode"],
+                    help="decode: time fs_decode (Alg 5 DPG plan) instead of the encode (NEXT-1)")
+    ap.add_argument("--recv-frac", type=float, default=0.95,
+                    help="decode: fraction of coded symbols received (seeded random subset)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.op == "decode" and "--config" not in sys.argv:
+        args.config = 5
     cfg = configs.get(args.config)
+    if args.op == "decode":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "decode reference arm not implemented"}))
+            return
+        run_decode(args, cfg)
+        return
 
     if args.impl == "reference":
         run_reference(args, cfg)
@@ -318,6 +330,65 @@ def main():
         print(json.dumps(out))
     if ws > 1:
         dist.destroy_process_group()
+
+
+def run_decode(args, cfg):
+    """NEXT-1: decode throughput of the Alg 5 (DPG) plan, one GPU.  The coded symbols come from one
+    (untimed) encode; a seeded random subset of them (--recv-frac) is 'received'; one step = one
+    fs_decode call (one launch per DPG level) over every stripe."""
+    import numpy as np
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    g = fsb.Graph.create(cfg)
+    k, p, n, t, S = cfg["k"], cfg["p"], cfg["n"], cfg["t"], cfg["stripes"]
+    K = k + p
+    data = inputs.stripe_data(cfg, device=dev)
+    chk = torch.empty((S, p, t), dtype=torch.uint8, device=dev) if p else None
+    cod = torch.empty((S, n, t), dtype=torch.uint8, device=dev)
+    g.encode_stripes(data, chk, cod)
+    recv = np.random.default_rng(cfg["seed"]).random(n) < args.recv_frac
+    plan = fsb.DecodePlan(g, recv)
+    inf = plan.info()
+    cod[:, torch.from_numpy(~recv).to(dev)] = 0                 # erased symbols
+    inter = torch.zeros((S, K, t), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    for _ in range(args.warmup):
+        plan.decode(cod, inter, stream=stream)
+    launches = fsb.last_launch_count()
+    stream.synchronize()
+    st, _ = plan.state()
+    rec = torch.from_numpy(st[:k].astype(bool)).to(dev)
+    ok = bool(torch.equal(inter[:, :k][:, rec], data[:, rec]))
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    with torch.cuda.stream(stream):
+        evs[0].record(stream)
+        for i in range(args.steps):
+            plan.decode(cod, inter, stream=stream)
+            evs[i + 1].record(stream)
+    stream.synchronize()
+    clk = clocks.stop()
+    ms = evs[0].elapsed_time(evs[-1]) / args.steps
+    rec_bytes = S * inf["recovered_data"] * t
+    value = rec_bytes / (ms * 1e-3) / 1e9
+    # one read of every coded row a plan row uses + one write of every recovered symbol
+    b_hbm = S * (int(recv.sum()) + inf["recovered"]) * t
+    peak, peak_src = _peaks()
+    out = {"op": "decode", "metric": "decode throughput, recovered data GB/s (Alg 5 DPG plan)",
+           "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(ms, 5), "higher_is_better": True, "dtype": "u8", "data": DATA,
+           "config": {"workload": cfg["name"], "k": k, "p": p, "n": n, "t": t, "stripes": S,
+                      "recv_frac": args.recv_frac, "received": int(recv.sum()),
+                      "recovered_data": inf["recovered_data"], "levels": inf["levels"],
+                      "xor_sources": inf["xor_sources"]},
+           "roofline": {"bound": "hbm", "achieved": round(b_hbm / (ms * 1e-3) / 1e9, 1), "peak": peak,
+                        "unit": "GB/s", "frac": round(b_hbm / (ms * 1e-3) / 1e9 / peak, 4),
+                        "algorithmic_bytes_per_step": b_hbm, "peak_source": peak_src,
+                        "kernel": "fsb_dpg_level x %d launches" % launches},
+           "gpu_launches": launches * args.steps, "checked": ok, "clocks": clk}
+    print(json.dumps(out))
 
 
 def _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all):
