@@ -146,11 +146,68 @@ static void draw_neighbours(uint64_t *st, uint32_t d, uint32_t range, int32_t *o
 /* ------------------------------------------------------------ graph (a1) */
 /* Generates the precode and LT neighbour lists.  lt_col capacity must be >= n * max_degree.
  * Returns the LT nnz, or -1 on error. */
+/* ------------------------------------------- array LDPC precode (Alg 2, NEXT-2) */
+static uint32_t largest_prime_factor(uint32_t x) {
+  uint32_t best = 1, d;
+  for (d = 2; (uint64_t)d * d <= x; ++d)
+    while (x % d == 0) { best = d; x /= d; }
+  return x > 1 ? x : best;
+}
+
+/* Algorithm 2 for the paper's (b, k) = (our k data symbols, our K = k+p):
+ *   P = largest_prime_factor(K), k' = K/P, j' = k' - b/P,
+ *   for j < j', i < P, m = 1..k'-j':  l[i+jP][m-1] = k'P - (j'-j+m-1)P - ((m(j'-j-1) - i - 1 + P) mod P) - 1
+ * with the mod taken as the non-negative residue (reading R18).  Row r lists the k'-j' members of
+ * check r (symbol indices in [0,K): data m < k, check m-k otherwise); the check symbol itself is
+ * index k+r, so the group {members, k+r} XORs to zero.  Realizable (Alg 3's conditions): P | b,
+ * j' >= 1, k' - j' >= 1, k' <= P.  Returns the members per check, or -1. */
+int32_t or_array_precode(uint32_t k, uint32_t K, int32_t *pre_row_ptr, int32_t *pre_col) {
+  uint32_t P, kp, jp, j, i, m, d, r = 0;
+  if (K <= k || k == 0) return -1;
+  P = largest_prime_factor(K);
+  if (P < 2 || k % P != 0) return -1;
+  kp = K / P;
+  jp = kp - k / P;
+  if (jp < 1 || kp <= jp || kp > P) return -1;
+  d = kp - jp;
+  pre_row_ptr[0] = 0;
+  for (j = 0; j < jp; ++j)
+    for (i = 0; i < P; ++i, ++r) {
+      for (m = 1; m <= d; ++m) {
+        int64_t inner = (int64_t)m * ((int64_t)jp - j - 1) - i - 1 + P;
+        int64_t res = ((inner % P) + P) % P;
+        int64_t v = (int64_t)kp * P - ((int64_t)jp - j + m - 1) * P - res - 1;
+        pre_col[(size_t)r * d + (m - 1)] = (int32_t)v;
+      }
+      pre_row_ptr[r + 1] = (int32_t)((r + 1) * d);
+    }
+  return (int32_t)d;
+}
+
+int64_t or_generate_graph_ex(uint32_t k, uint32_t p, uint32_t d_p, uint32_t n, uint64_t seed,
+                             int kind, double rsd_c, double rsd_delta,
+                             const uint32_t *fin_deg, const double *fin_prob, uint32_t fin_len,
+                             int precode_kind,
+                             int32_t *pre_row_ptr, int32_t *pre_col,
+                             int32_t *lt_row_ptr, int32_t *lt_col);
+
 int64_t or_generate_graph(uint32_t k, uint32_t p, uint32_t d_p, uint32_t n, uint64_t seed,
                           int kind, double rsd_c, double rsd_delta,
                           const uint32_t *fin_deg, const double *fin_prob, uint32_t fin_len,
                           int32_t *pre_row_ptr, int32_t *pre_col,
                           int32_t *lt_row_ptr, int32_t *lt_col) {
+  return or_generate_graph_ex(k, p, d_p, n, seed, kind, rsd_c, rsd_delta, fin_deg, fin_prob, fin_len, 0,
+                              pre_row_ptr, pre_col, lt_row_ptr, lt_col);
+}
+
+/* precode_kind 0: p random checks of d_p distinct data symbols drawn from the stream (R5, R11);
+ * 1: Alg 2 array LDPC checks (deterministic, no stream draws; d_p is implied).            */
+int64_t or_generate_graph_ex(uint32_t k, uint32_t p, uint32_t d_p, uint32_t n, uint64_t seed,
+                             int kind, double rsd_c, double rsd_delta,
+                             const uint32_t *fin_deg, const double *fin_prob, uint32_t fin_len,
+                             int precode_kind,
+                             int32_t *pre_row_ptr, int32_t *pre_col,
+                             int32_t *lt_row_ptr, int32_t *lt_col) {
   uint32_t K = k + p, i, j, len;
   uint64_t st = seed;
   int64_t nnz = 0;
@@ -158,17 +215,20 @@ int64_t or_generate_graph(uint32_t k, uint32_t p, uint32_t d_p, uint32_t n, uint
   double *cdf;
   int r;
   if (k == 0 || n == 0) return -1;
-  if (p > 0 && (d_p == 0 || d_p > k)) return -1;
+  if (precode_kind == 0 && p > 0 && (d_p == 0 || d_p > k)) return -1;
+  if (precode_kind == 1 && (p == 0 || or_array_precode(k, K, pre_row_ptr, pre_col) < 0)) return -1;
   deg = (uint32_t *)malloc(sizeof(uint32_t) * (K + fin_len + 1));
   cdf = (double *)malloc(sizeof(double) * (K + fin_len + 1));
   r = or_build_cdf(kind, K, rsd_c, rsd_delta, fin_deg, fin_prob, fin_len, deg, cdf);
   if (r < 0) { free(deg); free(cdf); return -1; }
   len = (uint32_t)r;
-  /* step (1): precode checks first (R5, R11) */
-  pre_row_ptr[0] = 0;
-  for (i = 0; i < p; ++i) {
-    draw_neighbours(&st, d_p, k, pre_col + (size_t)i * d_p);
-    pre_row_ptr[i + 1] = (int32_t)((i + 1) * d_p);
+  /* step (1): precode checks first (R5, R11); the array precode draws nothing */
+  if (precode_kind == 0) {
+    pre_row_ptr[0] = 0;
+    for (i = 0; i < p; ++i) {
+      draw_neighbours(&st, d_p, k, pre_col + (size_t)i * d_p);
+      pre_row_ptr[i + 1] = (int32_t)((i + 1) * d_p);
+    }
   }
   /* step (2): LT rows: one degree draw, then the neighbour draws (R5, R12) */
   lt_row_ptr[0] = 0;
@@ -204,11 +264,14 @@ void or_encode_stripe(uint32_t k, uint32_t p, uint32_t n, uint64_t t,
                       const uint8_t *data, uint8_t *checks, uint8_t *coded) {
   uint32_t i, j;
   int32_t e;
+  /* checks in row order: a member m >= k is an earlier check (array precode, Alg 2) */
   for (i = 0; i < p; ++i) {
     uint8_t *c = checks + (uint64_t)i * t;
     memset(c, 0, t);
-    for (e = pre_row_ptr[i]; e < pre_row_ptr[i + 1]; ++e)
-      xor_into(c, data + (uint64_t)pre_col[e] * t, t);
+    for (e = pre_row_ptr[i]; e < pre_row_ptr[i + 1]; ++e) {
+      uint32_t m = (uint32_t)pre_col[e];
+      xor_into(c, m < k ? data + (uint64_t)m * t : checks + (uint64_t)(m - k) * t, t);
+    }
   }
   for (j = 0; j < n; ++j) {
     uint8_t *y = coded + (uint64_t)j * t;

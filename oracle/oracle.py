@@ -39,6 +39,11 @@ def lib():
         L.or_generate_graph.argtypes = [u32, u32, u32, u32, u64, ctypes.c_int, dbl, dbl, P, P, u32,
                                         P, P, P, P]
         L.or_generate_graph.restype = i64
+        L.or_generate_graph_ex.argtypes = [u32, u32, u32, u32, u64, ctypes.c_int, dbl, dbl, P, P, u32,
+                                           ctypes.c_int, P, P, P, P]
+        L.or_generate_graph_ex.restype = i64
+        L.or_array_precode.argtypes = [u32, u32, P, P]
+        L.or_array_precode.restype = ctypes.c_int32
         L.or_encode_stripe.argtypes = [u32, u32, u32, u64, P, P, P, P, P, P, P]
         L.or_encode_stripe.restype = None
         L.or_encode_stripes.argtypes = [u32, u32, u32, u32, u64, P, P, P, P, P, u64, P, u64, P, u64]
@@ -93,9 +98,23 @@ class Graph:
         return self.pre_col[self.pre_row_ptr[i]:self.pre_row_ptr[i + 1]]
 
 
+def array_precode(k, K):
+    """Alg 2 check sets for k data of K symbols: (pre_row_ptr, pre_col)."""
+    pre_row_ptr = np.zeros(K - k + 1, dtype=np.int32)
+    pre_col = np.zeros(max(1, (K - k) * K), dtype=np.int32)
+    d = lib().or_array_precode(k, K, _p(pre_row_ptr), _p(pre_col))
+    if d < 0:
+        raise ValueError("array precode not realizable for (k=%d, K=%d)" % (k, K))
+    return pre_row_ptr, pre_col[:(K - k) * d].copy()
+
+
 def generate_graph(cfg):
-    """Graph generation a1 (readings R2-R15)."""
-    k, p, d_p, n = cfg["k"], cfg["p"], cfg["d_p"], cfg["n"]
+    """Graph generation a1 (readings R2-R15; NEXT-2: Alg 2 precode)."""
+    k, p, n = cfg["k"], cfg["p"], cfg["n"]
+    array = cfg.get("precode", "random") == "array"
+    d_p = cfg["d_p"]
+    if array:
+        d_p = int(np.diff(array_precode(k, k + p)[0])[0])
     K = k + p
     fd = np.ascontiguousarray(cfg.get("fin_deg", ()), dtype=np.uint32)
     fp = np.ascontiguousarray(cfg.get("fin_prob", ()), dtype=np.float64)
@@ -105,9 +124,9 @@ def generate_graph(cfg):
     pre_col = np.zeros(max(p * d_p, 1), dtype=np.int32)
     lt_row_ptr = np.zeros(n + 1, dtype=np.int32)
     lt_col = np.zeros(cap, dtype=np.int32)
-    nnz = lib().or_generate_graph(k, p, d_p, n, cfg["seed"], cfg["dist"], cfg.get("rsd_c", 0.0),
-                                  cfg.get("rsd_delta", 0.0), _p(fd), _p(fp), len(fd),
-                                  _p(pre_row_ptr), _p(pre_col), _p(lt_row_ptr), _p(lt_col))
+    nnz = lib().or_generate_graph_ex(k, p, d_p, n, cfg["seed"], cfg["dist"], cfg.get("rsd_c", 0.0),
+                                     cfg.get("rsd_delta", 0.0), _p(fd), _p(fp), len(fd), 1 if array else 0,
+                                     _p(pre_row_ptr), _p(pre_col), _p(lt_row_ptr), _p(lt_col))
     if nnz < 0:
         raise ValueError("invalid graph parameters")
     return Graph(cfg, pre_row_ptr, pre_col[:p * d_p].copy(), lt_row_ptr, lt_col[:nnz].copy())

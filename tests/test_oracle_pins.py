@@ -487,3 +487,93 @@ def test_paper_repair_example_xor_algebra():
     _, Dd = oracle.encode(g, Cs)
     lhs = Cs[2] ^ Cs[12] ^ Cs[17] ^ Cs[20] ^ Cs[21]
     assert np.array_equal(lhs, Dd[0] ^ Dd[1] ^ Dd[2])
+
+
+# --------------------------------------------------------- NEXT-2: array LDPC precode (Alg 2)
+ARRAY_CASES = [(3, 6), (962, 1036), (999, 1036), (837, 930), (34, 51)]
+
+
+def _lpf(x):
+    best, d = 1, 2
+    while d * d <= x:
+        while x % d == 0:
+            best, x = d, x // d
+        d += 1
+    return x if x > 1 else best
+
+
+def test_array_precode_golden_k6_b3():
+    """tests/golden/array_ldpc_k6_b3.txt: Alg 2 evaluated by hand."""
+    rp, col = oracle.array_precode(3, 6)
+    want = [[int(r[1])] for r in _golden_rows("array_ldpc_k6_b3.txt")]
+    got = [col[rp[i]:rp[i + 1]].tolist() for i in range(3)]
+    assert got == want
+
+
+@pytest.mark.parametrize("k,K", ARRAY_CASES)
+def test_array_precode_is_an_array_code(k, K):
+    """Array LDPC structure (\\cite{arrayldpc}): the check matrix is built from
+    P x P circulant permutation blocks -- for every block row j and member slot m, check i of
+    the block row hits one block of P consecutive symbols, and i -> offset is a cyclic shift.
+    Encodable in row order (linear-time): members are data or earlier checks."""
+    P = _lpf(K)
+    kp, jp = K // P, K // P - k // P
+    rp, col = oracle.array_precode(k, K)
+    d = kp - jp
+    assert len(rp) == K - k + 1 and np.all(np.diff(rp) == d)
+    rows = [col[rp[r]:rp[r + 1]] for r in range(K - k)]
+    for r, mem in enumerate(rows):
+        assert len(set(mem.tolist())) == d
+        assert np.all(mem >= 0) and np.all(mem < K)
+        assert np.all((mem < k) | (mem - k < r)), "references a later check"
+    for j in range(jp):
+        for m in range(d):
+            vals = np.array([rows[i + j * P][m] for i in range(P)])
+            blk = vals // P
+            assert len(set(blk.tolist())) == 1, "not one block"
+            off = vals % P
+            shift = (off - np.arange(P)) % P
+            assert len(set(shift.tolist())) == 1, "not a circulant permutation"
+
+
+@pytest.mark.parametrize("k,K", [c for c in ARRAY_CASES if (c[1] // _lpf(c[1])) <= _lpf(c[1])])
+def test_array_precode_has_no_four_cycles(k, K):
+    """Array codes with k' <= P (Alg 3's realizability condition) have girth >= 6: two check
+    groups (members + their own check symbol) share at most one symbol."""
+    rp, col = oracle.array_precode(k, K)
+    groups = [set(col[rp[r]:rp[r + 1]].tolist()) | {k + r} for r in range(K - k)]
+    inc = np.zeros((len(groups), K), dtype=np.int64)
+    for r, gset in enumerate(groups):
+        inc[r, list(gset)] = 1
+    share = inc @ inc.T
+    np.fill_diagonal(share, 0)
+    assert share.max() <= 1
+
+
+def test_array_precode_rejects_unrealizable():
+    for k, K in [(1000, 1020), (990, 1100), (5, 5), (0, 6)]:
+        with pytest.raises(ValueError):
+            oracle.array_precode(k, K)
+
+
+@pytest.mark.parametrize("k,K", ARRAY_CASES[:3])
+def test_array_precode_encoding_zero_syndrome(k, K):
+    """Every check group XORs to zero after encoding (SPEC.md Check1Sets invariant), and the
+    LT stage then reads the checks like data."""
+    cfg = dict(k=k, p=K - k, d_p=0, n=int(1.25 * K), t=64, dist=configs.FINITE, seed=5,
+               fin_deg=configs.OMEGA_DEGREES, fin_prob=configs.OMEGA_PROBS, precode="array", stripes=2)
+    g = oracle.generate_graph(cfg)
+    D = inputs.stripe_data(cfg).numpy()
+    C, Y = oracle.encode(g, D)
+    for s in range(2):
+        I = np.concatenate([D[s], C[s]])
+        for r in range(K - k):
+            acc = I[k + r].copy()
+            for m in g.pre_row(r):
+                acc ^= I[m]
+            assert not acc.any()
+        for j in range(0, g.n, 7):
+            acc = np.zeros(64, np.uint8)
+            for m in g.lt_row(j):
+                acc ^= I[m]
+            assert np.array_equal(acc, Y[s][j])
