@@ -63,6 +63,16 @@ typedef enum {
 
 typedef enum { FS_DIST_RSD = 1, FS_DIST_FINITE = 2 } fs_dist_kind;
 
+/* Precode kinds (PAPER.md:91 step (1), "Check #1").
+ * FS_PRECODE_RANDOM: p checks, each the XOR of d_p distinct data symbols drawn from the graph
+ *   stream (BASELINE.json configs; readings R5, R11).
+ * FS_PRECODE_ARRAY: the paper's binary array LDPC precode, Alg 2 (SURVEY.md
+ *   NEXT-2): for the paper's (b, k) = (k, k+p), P = largest prime factor of k+p, k' = (k+p)/P,
+ *   j' = k' - k/P; p = j'P checks of k'-j' members each (data symbols or EARLIER checks), no
+ *   stream draws; d_p is ignored (set to k'-j').  Realizable iff P divides k, j' >= 1,
+ *   k' > j' and k' <= P (Alg 3's conditions); otherwise FS_EINVAL.                           */
+typedef enum { FS_PRECODE_RANDOM = 0, FS_PRECODE_ARRAY = 1 } fs_precode_kind;
+
 /* Code parameters: the paper's problem statement. */
 typedef struct {
   uint32_t k;             /* data symbols (paper b); >= 1                                     */
@@ -77,6 +87,7 @@ typedef struct {
   const double *fin_prob;    /* FINITE: weights >= 0, sum within 1e-5 of 1 (normalised)      */
   uint32_t fin_len;          /* FINITE: number of support points                             */
   uint64_t seed;          /* splitmix64 graph seed (reading R2/R3)                            */
+  int32_t precode;        /* fs_precode_kind (0 = FS_PRECODE_RANDOM)                          */
 } fs_params;
 
 typedef struct fs_graph fs_graph;  /* opaque */
@@ -101,8 +112,9 @@ typedef struct fs_graph fs_graph;  /* opaque */
 FSB_API fs_status fs_graph_create(const fs_params *prm, uint32_t flags, fs_graph **out);
 
 /* Build a graph from CSR arrays (e.g. received by NCCL broadcast from rank 0).
- * pre_row_ptr[p+1], pre_col[p*d_p] (indices in [0,k)), lt_row_ptr[n+1], lt_col[nnz]
- * (indices in [0,K)); rows need not be sorted but must hold distinct indices.
+ * pre_row_ptr[p+1], pre_col[p*d_p] (indices in [0,k), or k+i' for an earlier check i' < i),
+ * lt_row_ptr[n+1], lt_col[nnz] (indices in [0,K)); rows need not be sorted but must hold
+ * distinct indices, and precode levels must not decrease with the row index.
  * The arrays are copied.  FS_EINVAL on any structural violation.                         */
 FSB_API fs_status fs_graph_from_csr(const fs_params *prm, const int32_t *pre_row_ptr,
                             const int32_t *pre_col, const int32_t *lt_row_ptr,

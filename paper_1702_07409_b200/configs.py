@@ -27,6 +27,11 @@ CONFIGS = {
             rsd_c=0.1, rsd_delta=0.05, seed=4, stripes=256),
     5: dict(name="c5_large_stripe", k=50000, p=500, d_p=4, n=60000, t=8192, dist=FINITE,
             seed=5, stripes=1),
+    # Not a BASELINE config: the NEXT-2 measurement workload -- config 4's shape (256 stripes of
+    # 4 KiB symbols, RSD(0.1, 0.05), n=1280) with the paper's array-LDPC precode (Alg 2) for
+    # (b, k) = (962, 1036): P=37, k'=28, j'=2, 74 checks of 26 members in 2 levels.
+    6: dict(name="c6_array_precode", k=962, p=74, d_p=26, n=1280, t=4096, dist=RSD,
+            rsd_c=0.1, rsd_delta=0.05, seed=6, stripes=256, precode="array"),
 }
 
 

@@ -20,6 +20,11 @@ namespace {
 
 fs_status finish_create(fs_graph *h, uint32_t flags, fs_graph **out) {
   fsb::Graph &g = h->g;
+  fs_status lv = fsb::build_precode_levels(g);
+  if (lv != FS_OK) {
+    delete h;
+    return lv;
+  }
   fsb::build_smem_schedule(g);
   if (!(flags & FS_GRAPH_HOST_ONLY)) {
     fs_status st = fsb::upload_graph(g);
@@ -96,6 +101,7 @@ fs_status fs_graph_from_csr(const fs_params *prm, const int32_t *pre_row_ptr, co
     g.pre_row_ptr.assign(pre_row_ptr, pre_row_ptr + p + 1);
     if (g.pre_row_ptr[p] < 0) { delete h; set_error("invalid precode CSR"); return FS_EINVAL; }
     g.pre_col.assign(pre_col, pre_col + g.pre_row_ptr[p]);
+    if (g.prm.precode == FS_PRECODE_ARRAY) g.prm.d_p = static_cast<uint32_t>(g.pre_row_ptr[1] - g.pre_row_ptr[0]);
   } else {
     g.pre_row_ptr.assign(1, 0);
   }

@@ -55,11 +55,45 @@ struct NeighbourSampler {
 
 }  // namespace
 
+// Largest prime factor by trial division (Alg 2's largest_prime_factor).
+uint32_t lpf(uint32_t x) {
+  uint32_t best = 1;
+  for (uint32_t d = 2; static_cast<uint64_t>(d) * d <= x; ++d)
+    while (x % d == 0) {
+      best = d;
+      x /= d;
+    }
+  return x > 1 ? x : best;
+}
+
+// Array LDPC shape for the paper's (b, k) = (k, K): {P, k', j'}; false if not realizable.
+bool array_shape(uint32_t k, uint32_t K, uint32_t &P, uint32_t &kp, uint32_t &jp) {
+  if (k == 0 || K <= k) return false;
+  P = lpf(K);
+  if (P < 2 || k % P) return false;
+  kp = K / P;
+  jp = kp - k / P;
+  return jp >= 1 && kp > jp && kp <= P;
+}
+
 fs_status validate_params(const fs_params &prm) {
   if (prm.k == 0 || prm.n == 0) { set_error("k and n must be >= 1"); return FS_EINVAL; }
+  if (prm.precode != FS_PRECODE_RANDOM && prm.precode != FS_PRECODE_ARRAY) {
+    set_error("unknown precode kind");
+    return FS_EINVAL;
+  }
+  if (prm.precode == FS_PRECODE_ARRAY) {
+    uint32_t P, kp, jp;
+    if (prm.p == 0 || static_cast<uint64_t>(prm.k) + prm.p >= (1ull << 31) ||
+        !array_shape(prm.k, prm.k + prm.p, P, kp, jp)) {
+      set_error("array precode not realizable: need P = largest prime factor of k+p dividing k, "
+                "j' = (k+p)/P - k/P >= 1 and k/P >= 1, (k+p)/P <= P");
+      return FS_EINVAL;
+    }
+  }
   if (prm.t == 0 || prm.t % 16 != 0) { set_error("t must be a positive multiple of 16"); return FS_EINVAL; }
   if (prm.t >= (1ull << 31)) { set_error("t must be below 2^31"); return FS_EINVAL; }
-  if (prm.p > 0 && (prm.d_p == 0 || prm.d_p > prm.k)) {
+  if (prm.precode == FS_PRECODE_RANDOM && prm.p > 0 && (prm.d_p == 0 || prm.d_p > prm.k)) {
     set_error("precode degree d_p must satisfy 1 <= d_p <= k");
     return FS_EINVAL;
   }
@@ -138,12 +172,33 @@ fs_status generate_csr(Graph &g) {
   const uint32_t k = prm.k, p = prm.p, n = prm.n, K = k + p;
   SplitMix64 rng(prm.seed);
   NeighbourSampler sampler(K);
-  // step (1): precode checks first (R5, R11)
+  // step (1): precode checks first (R5, R11); the array precode (Alg 2) draws nothing
   g.pre_row_ptr.assign(p + 1, 0);
-  g.pre_col.assign(static_cast<size_t>(p) * prm.d_p, 0);
-  for (uint32_t i = 0; i < p; ++i) {
-    sampler.draw(rng, prm.d_p, k, g.pre_col.data() + static_cast<size_t>(i) * prm.d_p);
-    g.pre_row_ptr[i + 1] = static_cast<int32_t>((i + 1) * prm.d_p);
+  if (prm.precode == FS_PRECODE_ARRAY) {
+    uint32_t P = 0, kp = 0, jp = 0;
+    array_shape(k, K, P, kp, jp);
+    const uint32_t d = kp - jp;
+    g.prm.d_p = d;
+    g.pre_col.assign(static_cast<size_t>(p) * d, 0);
+    // Alg 2: check i + jP, member slot m-1; mod = non-negative residue (R18).
+    // Member values index the K symbols: data m < k, check m-k (always an earlier check).
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < jp; ++j)
+      for (uint32_t i = 0; i < P; ++i, ++r) {
+        for (uint32_t m = 1; m <= d; ++m) {
+          const int64_t x = static_cast<int64_t>(m) * (static_cast<int64_t>(jp) - j - 1) - i - 1 + P;
+          const int64_t res = ((x % P) + P) % P;
+          g.pre_col[static_cast<size_t>(r) * d + m - 1] = static_cast<int32_t>(
+              static_cast<int64_t>(kp) * P - (static_cast<int64_t>(jp) - j + m - 1) * P - res - 1);
+        }
+        g.pre_row_ptr[r + 1] = static_cast<int32_t>((r + 1) * d);
+      }
+  } else {
+    g.pre_col.assign(static_cast<size_t>(p) * prm.d_p, 0);
+    for (uint32_t i = 0; i < p; ++i) {
+      sampler.draw(rng, prm.d_p, k, g.pre_col.data() + static_cast<size_t>(i) * prm.d_p);
+      g.pre_row_ptr[i + 1] = static_cast<int32_t>((i + 1) * prm.d_p);
+    }
   }
   // step (2): LT rows, one degree draw then the neighbour draws (R5, R12)
   g.lt_row_ptr.assign(n + 1, 0);
@@ -172,16 +227,19 @@ fs_status validate_csr(const Graph &g) {
   if (g.pre_row_ptr.size() != p + 1 || g.lt_row_ptr.size() != n + 1) { set_error("CSR row_ptr size"); return FS_EINVAL; }
   std::vector<uint32_t> seen(K, 0);
   uint32_t epoch = 0;
+  // precode row r: members are data (< k) or earlier checks (k + r' with r' < r)
   auto check_rows = [&](const std::vector<int32_t> &rp, const std::vector<int32_t> &col, uint32_t rows,
-                        uint32_t range, bool fixed_deg) -> bool {
+                        bool precode) -> bool {
     if (rp[0] != 0) return false;
     for (uint32_t r = 0; r < rows; ++r) {
       if (rp[r + 1] < rp[r] || static_cast<size_t>(rp[r + 1]) > col.size()) return false;
       if (rp[r + 1] == rp[r]) return false;  // every row has degree >= 1
-      if (fixed_deg && static_cast<uint32_t>(rp[r + 1] - rp[r]) != g.prm.d_p) return false;
+      if (precode && g.prm.precode == FS_PRECODE_RANDOM && static_cast<uint32_t>(rp[r + 1] - rp[r]) != g.prm.d_p)
+        return false;
       ++epoch;
       for (int32_t e = rp[r]; e < rp[r + 1]; ++e) {
         const int32_t m = col[e];
+        const uint32_t range = precode ? k + r : K;
         if (m < 0 || static_cast<uint32_t>(m) >= range) return false;
         if (seen[m] == epoch) return false;
         seen[m] = epoch;
@@ -189,8 +247,33 @@ fs_status validate_csr(const Graph &g) {
     }
     return static_cast<size_t>(rp[rows]) == col.size();
   };
-  if (!check_rows(g.pre_row_ptr, g.pre_col, p, k, true)) { set_error("invalid precode CSR"); return FS_EINVAL; }
-  if (!check_rows(g.lt_row_ptr, g.lt_col, n, K, false)) { set_error("invalid LT CSR"); return FS_EINVAL; }
+  if (!check_rows(g.pre_row_ptr, g.pre_col, p, true)) { set_error("invalid precode CSR"); return FS_EINVAL; }
+  if (!check_rows(g.lt_row_ptr, g.lt_col, n, false)) { set_error("invalid LT CSR"); return FS_EINVAL; }
+  return FS_OK;
+}
+
+// Precode levels: a check reading only data is level 0, else 1 + the largest level of the
+// checks it reads.  The kernels compute one level at a time, so levels must not decrease with
+// the row index (true for the random precode, one level, and for Alg 2, level = block row j).
+fs_status build_precode_levels(Graph &g) {
+  const uint32_t k = g.prm.k, p = g.prm.p;
+  std::vector<uint32_t> level(p, 0);
+  g.pre_level_ptr.assign(1, 0);
+  uint32_t cur = 0;
+  for (uint32_t r = 0; r < p; ++r) {
+    uint32_t L = 0;
+    for (int32_t e = g.pre_row_ptr[r]; e < g.pre_row_ptr[r + 1]; ++e) {
+      const uint32_t m = static_cast<uint32_t>(g.pre_col[e]);
+      if (m >= k) L = std::max(L, level[m - k] + 1);
+    }
+    level[r] = L;
+    if (r > 0 && L < cur) { set_error("precode levels must not decrease with the row index"); return FS_EINVAL; }
+    while (cur < L) {
+      g.pre_level_ptr.push_back(r);
+      ++cur;
+    }
+  }
+  g.pre_level_ptr.push_back(p);
   return FS_OK;
 }
 
@@ -223,7 +306,7 @@ void build_smem_schedule(Graph &g) {
     return static_cast<uint16_t>(r);
   };
   s.pre_slots.resize(g.pre_col.size());
-  for (size_t e = 0; e < g.pre_col.size(); ++e) s.pre_slots[e] = static_cast<uint16_t>(g.pre_col[e]);
+  for (size_t e = 0; e < g.pre_col.size(); ++e) s.pre_slots[e] = slot(g.pre_col[e]);  // data or earlier check
 
   struct Pair {                      // one group: half 0 (A) and half 1 (B)
     uint16_t row[2] = {kNoRow, kNoRow};

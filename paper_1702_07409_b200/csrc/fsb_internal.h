@@ -17,7 +17,8 @@ constexpr int kUnitRows = 64;
 constexpr int kUnitBytes = kUnitRows * kSliceBytes;     // 4 KiB
 constexpr int kConsumerWarps = 20;
 constexpr int kHalvesPerWarp = 8;                        // half-groups: 4 lanes x 16 B = 64 B
-constexpr int kThreads = (kConsumerWarps + 1) * 32;      // + 1 producer warp (TMA + precode)
+constexpr int kPrecodeWarps = 3;                         // precode (a3) warps per CTA
+constexpr int kThreads = (kConsumerWarps + 1 + kPrecodeWarps) * 32;  // + 1 TMA warp
 constexpr int kSplitThreshold = 48;                      // rows of degree > this are split:
 constexpr int kSplit2Max = 96;                           //   over the 2 halves of a group (<= this)
                                                          //   or over the 8 half-groups of a warp
@@ -78,6 +79,7 @@ struct DeviceBufs {
   uint32_t *sched = nullptr;
   uint32_t *warp_info = nullptr;
   uint16_t *pre_slots = nullptr;
+  uint32_t *pre_level_ptr = nullptr;
 };
 
 struct Graph {
@@ -85,6 +87,7 @@ struct Graph {
   std::vector<uint32_t> fin_deg;
   std::vector<double> fin_prob;
   std::vector<int32_t> pre_row_ptr, pre_col, lt_row_ptr, lt_col;
+  std::vector<uint32_t> pre_level_ptr;  // precode levels: checks [lp[L], lp[L+1]) read checks < lp[L]
   uint32_t max_degree = 0;
   bool smem_eligible = false;
   SmemSchedule sched;
@@ -100,6 +103,7 @@ fs_status validate_params(const fs_params &prm);
 fs_status build_cdf(const fs_params &prm, std::vector<uint32_t> &deg, std::vector<double> &cdf);
 fs_status generate_csr(Graph &g);
 fs_status validate_csr(const Graph &g);
+fs_status build_precode_levels(Graph &g);
 void build_smem_schedule(Graph &g);
 
 // fsb_kernels.cu

@@ -110,7 +110,9 @@ __device__ unsigned long long g_debug_counters[2 * 32];
 struct SmemArgs {
   const uint4 *sched;          // heads ++ conts chunk streams (fsb_internal.h: SmemSchedule)
   const uint32_t *warp_info;   // kConsumerWarps x {items, head_off, cont_off}
-  const uint16_t *pre_slots;   // p * d_p data rows
+  const uint16_t *pre_slots;   // p * d_p tile rows (data, or an earlier check)
+  const uint32_t *pre_level_ptr;  // precode levels (nlevels+1 row offsets)
+  uint32_t pre_levels;
   uint8_t *checks;
   uint64_t checks_stride;
   uint8_t *coded;
@@ -232,7 +234,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t T = a.tile_units;
   const uint32_t buf_bytes = T * kUnitBytes;
   uint8_t *sched_s = smem + 2 * static_cast<size_t>(buf_bytes);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sched_s + static_cast<size_t>(a.sched_chunks) * kChunkBytes);
+  uint16_t *pre_s = reinterpret_cast<uint16_t *>(sched_s + static_cast<size_t>(a.sched_chunks) * kChunkBytes);
+  const uint32_t pre_n = a.p * a.d_p;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(pre_s) + ((pre_n * 2 + 15) & ~15u));
   uint64_t *full = bars, *ready = bars + 2, *empty = bars + 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t smem_base = smem_u32(smem);
@@ -248,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the schedule (identical for every tile) and the two zero rows of each buffer
   for (uint32_t x = threadIdx.x; x < a.sched_chunks * (kChunkBytes / 16); x += blockDim.x)
     sts128(smem_u32(sched_s) + x * 16, __ldg(a.sched + x));
+  for (uint32_t x = threadIdx.x; x < pre_n; x += blockDim.x) pre_s[x] = __ldg(&a.pre_slots[x]);
   if (threadIdx.x < 2 * 2 * (kSliceBytes / 16)) {  // 2 buffers x 2 rows x 4 lanes
     const uint32_t b = threadIdx.x >> 3, r = (threadIdx.x >> 2) & 1, l4 = threadIdx.x & 3;
     sts128(smem_base + b * buf_bytes + (a.zero_even + r) * kSliceBytes + l4 * 16, make_uint4(0, 0, 0, 0));
@@ -255,37 +260,68 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    // ------------------------------------------------------- producer: TMA + precode checks
-    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-    const uint32_t half_id = lane >> 2, lane4 = lane & 3;
+    // ---------------------------------------------------------------- TMA warp (one lane)
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      uint32_t i = 0;
+      for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
+        const uint32_t b = i & 1, ph = (i >> 1) & 1;
+        const uint32_t stripe = tile / a.nslices, slice = tile % a.nslices;
+        const uint32_t buf = smem_base + b * buf_bytes;
+        mbar_wait(smem_u32(&empty[b]), ph ^ 1);  // consumers released tile i-2
+        if (a.debug & 1) {  // experiment: no TMA (consumers gather stale rows)
+          mbar_arrive(smem_u32(&full[b]));
+        } else {
+          mbar_arrive_expect_tx(smem_u32(&full[b]), a.data_units * kUnitBytes);
+        }
+        for (uint32_t u = 0; u < a.data_units && !(a.debug & 1); ++u)
+          tma_load_3d(buf + u * kUnitBytes, &tmap, smem_u32(&full[b]), static_cast<int32_t>(slice * kSliceBytes),
+                      static_cast<int32_t>(u * kUnitRows), static_cast<int32_t>(stripe));
+      }
+    }
+    return;
+  }
+  if (warp > kConsumerWarps) {
+    // ----------------------------------------------------------- precode warps (a3, Check #1)
+    // After a tile's rows land: its p checks (PAPER.md:91 step (1)) from shared memory into the
+    // buffer's check rows and to HBM, level by level (Alg 2 checks read earlier checks), then
+    // `ready`.  Separate from the TMA warp so the next tile's loads never wait for this work.
+    const uint32_t pw = warp - kConsumerWarps - 1;                  // precode warp 0..kPrecodeWarps-1
+    const uint32_t half_id = pw * kHalvesPerWarp + (lane >> 2), lane4 = lane & 3;
     uint32_t i = 0;
     for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
       const uint32_t b = i & 1, ph = (i >> 1) & 1;
       const uint32_t stripe = tile / a.nslices, slice = tile % a.nslices;
       const uint32_t buf = smem_base + b * buf_bytes;
-      if (lane == 0) {
-        mbar_wait(smem_u32(&empty[b]), ph ^ 1);  // consumers released tile i-2
-        mbar_arrive_expect_tx(smem_u32(&full[b]), a.data_units * kUnitBytes);
-        for (uint32_t u = 0; u < a.data_units; ++u)
-          tma_load_3d(buf + u * kUnitBytes, &tmap, smem_u32(&full[b]), static_cast<int32_t>(slice * kSliceBytes),
-                      static_cast<int32_t>(u * kUnitRows), static_cast<int32_t>(stripe));
-      }
-      __syncwarp();
       mbar_wait(smem_u32(&full[b]), ph);
-      // precode: check c by half-group c % 8, 16 B per lane
+      // precode, level by level (a check may read checks of earlier levels, Alg 2): check c of
+      // a level by half-group (c - level start) % 8, 16 B per lane
       const uint32_t lb = buf + lane4 * 16;
       const uint64_t col_off = static_cast<uint64_t>(slice) * kSliceBytes + lane4 * 16;
-      for (uint32_t c = half_id; c < a.p; c += kHalvesPerWarp) {
-        uint4 acc = make_uint4(0, 0, 0, 0);
-        for (uint32_t e = 0; e < a.d_p; ++e) {
-          const uint32_t r = __ldg(&a.pre_slots[c * a.d_p + e]);
-          xor_into(acc, lds128(lb + r * kSliceBytes));
+      for (uint32_t L = 0; L < a.pre_levels; ++L) {
+        const uint32_t c0 = __ldg(&a.pre_level_ptr[L]), c1 = __ldg(&a.pre_level_ptr[L + 1]);
+        for (uint32_t c = c0 + half_id; c < c1; c += kHalvesPerWarp * kPrecodeWarps) {
+          uint4 acc = make_uint4(0, 0, 0, 0);
+          const uint16_t *ps = pre_s + c * a.d_p;  // member rows, staged in shared memory
+          uint32_t e = 0;
+          for (; e + 8 <= a.d_p; e += 8) {  // 8 slot loads, then 8 gathers, in flight together
+            uint32_t r[8];
+            uint4 x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) r[u] = ps[e + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = lds128(lb + r[u] * kSliceBytes);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) xor_into(acc, x[u]);
+          }
+          for (; e < a.d_p; ++e) xor_into(acc, lds128(lb + ps[e] * kSliceBytes));
+          sts128(lb + (a.kpad + c) * kSliceBytes, acc);
+          st_stream(a.checks + stripe * a.checks_stride + c * a.t + col_off, acc);
         }
-        sts128(lb + (a.kpad + c) * kSliceBytes, acc);
-        st_stream(a.checks + stripe * a.checks_stride + c * a.t + col_off, acc);
+        // this level's check rows before the next level reads them (all precode warps)
+        asm volatile("bar.sync 2, %0;" ::"n"(kPrecodeWarps * 32) : "memory");
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&ready[b]));  // release: data + checks visible
+      if (pw == 0 && lane == 0) mbar_arrive(smem_u32(&ready[b]));  // release: data + checks visible
     }
     return;
   }
@@ -330,25 +366,30 @@ constexpr int kGlobalThreads = 256;
 constexpr int kGroupsPerBlock = kGlobalThreads / 8;
 constexpr uint32_t kGSliceBytes = 128;  // one 8-lane group = 8 x 16 B
 
+// Checks [c0, c0 + nc) of one precode level: one 8-lane group per (stripe, check, 128-B slice).
+// A member m >= k is a check of an earlier level (Alg 2), read from the checks buffer.
 __global__ void __launch_bounds__(kGlobalThreads)
-    fsb_precode_global(uint32_t S, uint32_t p, uint32_t d_p, uint64_t t, uint32_t nslices,
-                       const int32_t *__restrict__ pre_col, const uint8_t *__restrict__ data,
-                       uint64_t data_stride, uint8_t *__restrict__ checks, uint64_t checks_stride) {
+    fsb_precode_global(uint32_t S, uint32_t c0, uint32_t nc, uint32_t k, uint32_t d_p, uint64_t t,
+                       uint32_t nslices, const int32_t *__restrict__ pre_col, const uint8_t *__restrict__ data,
+                       uint64_t data_stride, uint8_t *checks, uint64_t checks_stride) {
   const uint64_t item = static_cast<uint64_t>(blockIdx.x) * kGroupsPerBlock + (threadIdx.x >> 3);
   const uint32_t lane8 = threadIdx.x & 7;
-  const uint64_t total = static_cast<uint64_t>(S) * p * nslices;
+  const uint64_t total = static_cast<uint64_t>(S) * nc * nslices;
   if (item >= total) return;
   const uint32_t slice = item % nslices;
   const uint64_t r = item / nslices;
-  const uint32_t c = r % p;
-  const uint32_t s = static_cast<uint32_t>(r / p);
+  const uint32_t c = c0 + static_cast<uint32_t>(r % nc);
+  const uint32_t s = static_cast<uint32_t>(r / nc);
   const uint64_t byte = static_cast<uint64_t>(slice) * kGSliceBytes + lane8 * 16;
   if (byte >= t) return;
   const uint8_t *src = data + s * data_stride + byte;
+  const uint8_t *csrc = checks + s * checks_stride + byte;
   uint4 acc = make_uint4(0, 0, 0, 0);
   for (uint32_t e = 0; e < d_p; ++e) {
-    const int32_t m = __ldg(&pre_col[c * d_p + e]);
-    xor_into(acc, __ldg(reinterpret_cast<const uint4 *>(src + static_cast<uint64_t>(m) * t)));
+    const uint32_t m = static_cast<uint32_t>(__ldg(&pre_col[c * d_p + e]));
+    const uint4 *p = reinterpret_cast<const uint4 *>(m < k ? src + static_cast<uint64_t>(m) * t
+                                                           : csrc + static_cast<uint64_t>(m - k) * t);
+    xor_into(acc, m < k ? __ldg(p) : *p);  // checks were written by an earlier launch
   }
   *reinterpret_cast<uint4 *>(checks + s * checks_stride + static_cast<uint64_t>(c) * t + byte) = acc;
 }
@@ -533,6 +574,7 @@ void free_device(Graph &g) {
   cudaFree(d.sched);
   cudaFree(d.warp_info);
   cudaFree(d.pre_slots);
+  cudaFree(d.pre_level_ptr);
   if (prev >= 0) cudaSetDevice(prev);
   d = DeviceBufs();
 }
@@ -557,8 +599,9 @@ fs_status upload_graph(Graph &g) {
     if ((st = upload(&g.dev.lt_colf, colf.data(), colf.size())) != FS_OK) return st;
   }
   if (g.smem_eligible) {
-    // two tile buffers + the schedule + 6 mbarriers
-    const uint64_t bytes = 2ull * g.sched.tile_units * kUnitBytes + g.sched.words.size() * 4 + 6 * 8;
+    // two tile buffers + the schedule + the precode member rows + 6 mbarriers
+    const uint64_t bytes = 2ull * g.sched.tile_units * kUnitBytes + g.sched.words.size() * 4 +
+                           ((g.sched.pre_slots.size() * 2 + 15) & ~15ull) + 6 * 8;
     g.smem_bytes = static_cast<uint32_t>(bytes);
     if (bytes > static_cast<uint64_t>(g.smem_optin)) {
       g.smem_eligible = false;
@@ -566,6 +609,7 @@ fs_status upload_graph(Graph &g) {
       if ((st = upload(&g.dev.sched, g.sched.words.data(), g.sched.words.size())) != FS_OK) return st;
       if ((st = upload(&g.dev.warp_info, g.sched.warp_info.data(), g.sched.warp_info.size())) != FS_OK) return st;
       if ((st = upload(&g.dev.pre_slots, g.sched.pre_slots.data(), g.sched.pre_slots.size())) != FS_OK) return st;
+      if ((st = upload(&g.dev.pre_level_ptr, g.pre_level_ptr.data(), g.pre_level_ptr.size())) != FS_OK) return st;
       e = cudaFuncSetAttribute(fsb_smem_encode, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(g.smem_bytes));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
@@ -613,6 +657,8 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     a.sched = reinterpret_cast<const uint4 *>(g.dev.sched);
     a.warp_info = g.dev.warp_info;
     a.pre_slots = g.dev.pre_slots;
+    a.pre_level_ptr = g.dev.pre_level_ptr;
+    a.pre_levels = static_cast<uint32_t>(g.pre_level_ptr.size() - 1);
     a.checks = checks;
     a.checks_stride = checks_stride;
     a.coded = coded;
@@ -647,11 +693,12 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     return FS_OK;
   }
   const uint32_t gslices = static_cast<uint32_t>((prm.t + kGSliceBytes - 1) / kGSliceBytes);
-  if (prm.p) {
-    const uint64_t items = static_cast<uint64_t>(S) * prm.p * gslices;
+  for (size_t L = 0; prm.p && L + 1 < g.pre_level_ptr.size(); ++L) {  // one launch per precode level
+    const uint32_t c0 = g.pre_level_ptr[L], nc = g.pre_level_ptr[L + 1] - c0;
+    const uint64_t items = static_cast<uint64_t>(S) * nc * gslices;
     const uint64_t blocks = (items + kGroupsPerBlock - 1) / kGroupsPerBlock;
     fsb_precode_global<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, prm.p, prm.d_p, prm.t, gslices, g.dev.pre_col, data, data_stride, checks, checks_stride);
+        S, c0, nc, prm.k, prm.d_p, prm.t, gslices, g.dev.pre_col, data, data_stride, checks, checks_stride);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_precode_global launch");
     ++*launches;
   }

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libfsb200.so")
 
 FS_OK, FS_EINVAL, FS_EDIST, FS_ENOMEM, FS_ECUDA, FS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 FS_DIST_RSD, FS_DIST_FINITE = 1, 2
+FS_PRECODE_RANDOM, FS_PRECODE_ARRAY = 0, 1
 FS_GRAPH_HOST_ONLY = 1
 VARIANT_AUTO, VARIANT_SMEM, VARIANT_GLOBAL = 0, 1, 2
 
@@ -37,7 +38,7 @@ class fs_params(ctypes.Structure):
                 ("rsd_c", ctypes.c_double), ("rsd_delta", ctypes.c_double),
                 ("fin_deg", ctypes.POINTER(ctypes.c_uint32)),
                 ("fin_prob", ctypes.POINTER(ctypes.c_double)), ("fin_len", ctypes.c_uint32),
-                ("seed", ctypes.c_uint64)]
+                ("seed", ctypes.c_uint64), ("precode", ctypes.c_int32)]
 
 
 class fs_graph_info(ctypes.Structure):
@@ -142,6 +143,7 @@ def make_params(cfg):
         prm.fin_prob = fp.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
     prm.fin_len = len(fd)
     prm.seed = cfg["seed"]
+    prm.precode = {"random": FS_PRECODE_RANDOM, "array": FS_PRECODE_ARRAY}[cfg.get("precode", "random")]
     return prm
 
 
@@ -153,6 +155,7 @@ class Graph:
         self.cfg = dict(cfg)
         self.k, self.p, self.n, self.t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
         self.d_p = cfg.get("d_p", 0)
+        self.precode = cfg.get("precode", "random")
         self.K = self.k + self.p
 
     @classmethod
@@ -187,7 +190,7 @@ class Graph:
             return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_int32)), (n,)).copy()
 
         pre_rp = arr(ptrs[0], self.p + 1)
-        pre_c = arr(ptrs[1], self.p * self.d_p if self.p else 0)
+        pre_c = arr(ptrs[1], int(pre_rp[-1]) if self.p else 0)
         lt_rp = arr(ptrs[2], self.n + 1)
         lt_c = arr(ptrs[3], int(nnz.value))
         return pre_rp, pre_c, lt_rp, lt_c

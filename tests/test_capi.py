@@ -234,3 +234,42 @@ def test_smem_schedule_covers_every_edge(cid):
     for j in range(c["n"]):
         want = sorted(m if m < k else kpad + (m - k) for m in lt_c[lt_rp[j]:lt_rp[j + 1]])
         assert rows[j] == want
+
+
+ARRAY_CFGS = [
+    dict(k=962, p=74, d_p=0, n=1280, t=4096, dist=configs.RSD, rsd_c=0.1, rsd_delta=0.05, seed=6),
+    dict(k=837, p=93, d_p=0, n=1100, t=128, dist=configs.FINITE, seed=7,
+         fin_deg=configs.OMEGA_DEGREES, fin_prob=configs.OMEGA_PROBS),
+    dict(k=3, p=3, d_p=0, n=9, t=16, dist=configs.FINITE, seed=8, fin_deg=(1, 2), fin_prob=(0.5, 0.5)),
+]
+
+
+@pytest.mark.parametrize("i", range(len(ARRAY_CFGS)))
+def test_array_precode_library_matches_oracle(i):
+    """NEXT-2: the library's Alg 2 precode + LT rows are byte-identical to the oracle's."""
+    c = dict(ARRAY_CFGS[i], precode="array")
+    g = fsb.Graph.create(c, host_only=True)
+    go = oracle.generate_graph(c)
+    pre_rp, pre_c, lt_rp, lt_c = g.csr()
+    assert np.array_equal(pre_rp, go.pre_row_ptr) and np.array_equal(pre_c, go.pre_col)
+    assert np.array_equal(lt_rp, go.lt_row_ptr) and np.array_equal(lt_c, go.lt_col)
+    inf = g.info()
+    assert inf["pre_nnz"] == len(pre_c) and inf["d_p"] == int(pre_rp[1])
+
+
+def test_array_precode_validation():
+    for k, p in [(1000, 20), (990, 110), (500, 100)]:   # P does not divide k, or k' > P
+        c = dict(ARRAY_CFGS[0], k=k, p=p, precode="array")
+        with pytest.raises(fsb.FsError) as e:
+            fsb.Graph.create(c, host_only=True)
+        assert e.value.status == fsb.FS_EINVAL
+    # a CSR whose check reads a LATER check is rejected; the Alg 2 CSR round-trips
+    c = dict(ARRAY_CFGS[0], precode="array")
+    g = fsb.Graph.create(c, host_only=True)
+    pre_rp, pre_c, lt_rp, lt_c = g.csr()
+    g2 = fsb.Graph.from_csr(c, pre_rp, pre_c, lt_rp, lt_c, host_only=True)
+    assert all(np.array_equal(a, b) for a, b in zip(g.csr(), g2.csr()))
+    bad = pre_c.copy()
+    bad[0] = c["k"] + 5                                  # check 0 reading check 5
+    with pytest.raises(fsb.FsError):
+        fsb.Graph.from_csr(c, pre_rp, bad, lt_rp, lt_c, host_only=True)

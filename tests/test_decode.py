@@ -125,3 +125,16 @@ def test_gpu_decode_matches_oracle(cid, frac, S):
         if c["p"]:
             chk_rec = rec[c["k"]:]
             assert np.array_equal(I[s][c["k"]:][chk_rec], C[s][chk_rec])
+
+
+def test_plan_with_array_precode_matches_oracle():
+    """Decoding through Alg 2 checks (checks whose members include earlier checks)."""
+    c = dict(configs.get(6), n=1150)
+    recv = _recv(c["n"], 0.97, 5)
+    g = fsb.Graph.create(c, host_only=True)
+    st, _ = fsb.DecodePlan(g, recv, host_only=True).state()
+    go = oracle.generate_graph(c)
+    D = inputs.stripe_data(c, num_stripes=1).numpy()[0]
+    _, Y = oracle.encode(go, D)
+    _, ostate = oracle.decode(go, recv, Y, use_elim=False)
+    assert np.array_equal(st, (ostate == 1).astype(np.uint8))

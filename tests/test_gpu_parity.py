@@ -272,3 +272,20 @@ def test_random_parameters(seed):
         if p:
             _assert_equal(c, C, "seed %d checks v%d" % (seed, v))
         _assert_equal(y, Y, "seed %d coded v%d" % (seed, v))
+
+
+@pytest.mark.parametrize("S", [1, 300])
+def test_array_precode_parity(S):
+    """NEXT-2: the Alg 2 precode (2 levels, checks reading checks) on both variants, bit-exact."""
+    _need_gpu()
+    cfg = dict(configs.get(6), stripes=S)
+    go = oracle.generate_graph(cfg)
+    D = inputs.stripe_data(cfg).numpy()
+    C, Y = oracle.encode(go, D)
+    variants = [fsb.VARIANT_AUTO, fsb.VARIANT_GLOBAL]
+    if fsb.Graph.create(cfg).info()["smem_eligible"]:
+        variants.append(fsb.VARIANT_SMEM)
+    for v in variants:
+        _, c, y = _run(cfg, v, data=torch.from_numpy(D).cuda())
+        _assert_equal(c, C, "array checks v%d" % v)
+        _assert_equal(y, Y, "array coded v%d" % v)

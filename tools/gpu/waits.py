@@ -4,7 +4,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 import torch
 from paper_1702_07409_b200 import configs, fsb, inputs
-cfg = configs.get(4)
+cfg = configs.get(int(sys.argv[1]) if len(sys.argv) > 1 else 4)
 g = fsb.Graph.create(cfg)
 S, k, p, n, t = cfg["stripes"], cfg["k"], cfg["p"], cfg["n"], cfg["t"]
 d = inputs.stripe_data(cfg, device="cuda")
