@@ -256,6 +256,7 @@ def main():
     clocks.start()
     time.sleep(0.3)
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    torch.cuda.nvtx.range_push("timed")   # ncu --nvtx --nvtx-include "timed/" captures only this
     with torch.cuda.stream(stream):
         evs[0].record(stream)
         for i in range(args.steps):
@@ -263,6 +264,7 @@ def main():
             evs[i + 1].record(stream)
     stream.synchronize()
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     if ws > 1:
         dist.barrier()
     clk = clocks.stop()

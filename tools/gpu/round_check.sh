@@ -21,6 +21,6 @@ for c in 5 3 2; do
 done
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 0"
 $CMD > $OUT/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" -c 400 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:fsb_ -s 3 -c 1 -o $OUT/prof_c4 $CMD > $OUT/ncu_full.log 2>&1
 echo "ncu rc=$?"
