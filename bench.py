@@ -124,10 +124,14 @@ def _dist_env():
     return ws, rank, local
 
 
-def plan(cfg, ws, rank, scaling):
-    """This rank's work: ("stripes", first stripe, count) or ("rows", row_begin, row_end)."""
+def plan(cfg, ws, rank, scaling, partition="rows"):
+    """This rank's work: ("stripes", first stripe, count), ("rows", row_begin, row_end) or
+    ("cols", col_begin, col_end) -- the last two split one large stripe (R16 / NEXT-4)."""
     S_total = cfg["stripes"]
     if S_total == 1 and ws > 1:
+        if partition == "cols":
+            c0, c1 = fdist.col_shard(cfg["t"], ws, rank)
+            return "cols", c0, c1
         r0, r1 = fdist.shard(cfg["n"], ws, rank)
         return "rows", r0, r1
     if scaling == "weak":
@@ -191,6 +195,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
     ap.add_argument("--variant", default="auto", choices=["auto", "smem", "global"])
+    ap.add_argument("--partition", default="rows", choices=["rows", "cols"],
+                    help="single-stripe configs at N>1: split coded rows (source replicated, BASELINE "
+                         "config 5) or byte columns (fs_encode_range, nothing replicated)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
@@ -226,11 +233,15 @@ def main():
         g = fsb.Graph.create(cfg)
     if args.variant != "auto":
         g.set_variant(fsb.VARIANT_SMEM if args.variant == "smem" else fsb.VARIANT_GLOBAL)
-    kind, u0, u1 = plan(cfg, ws, rank, args.scaling)
+    kind, u0, u1 = plan(cfg, ws, rank, args.scaling, args.partition)
     k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    cols = t
     if kind == "stripes":
         S, rows = u1, n
         data = inputs.stripe_data(cfg, stripe_begin=u0, num_stripes=S, device=dev)
+    elif kind == "cols":
+        S, rows, cols = 1, n, u1 - u0
+        data = inputs.stripe_data(cfg, device=dev)       # only bytes [u0, u1) are read
     else:
         S, rows = 1, u1 - u0
         data = inputs.stripe_data(cfg, device=dev)       # the source is replicated (R16)
@@ -242,6 +253,8 @@ def main():
     def step():
         if kind == "stripes":
             g.encode_stripes(data, chk, cod, stream=stream)
+        elif kind == "cols":
+            g.encode_range(data[0], chk[0] if p else None, cod[0], 0, n, u0, u1, stream=stream)
         else:
             g.encode(data[0], chk[0] if p else None, cod[0], u0, u1, stream=stream)
 
@@ -281,8 +294,8 @@ def main():
     # roofline of the dominant kernel (this rank): algorithmic HBM bytes per launch (one read of
     # the source, one write of checks + coded rows) / mean step time on the stream
     inf = g.info()
-    b_hbm = S * (k + p + rows) * t
-    b_gather = S * (inf["lt_nnz"] * rows // n + inf["pre_nnz"]) * t
+    b_hbm = S * (k + p + rows) * cols
+    b_gather = S * (inf["lt_nnz"] * rows // n + inf["pre_nnz"]) * cols
     launch_ms = statistics.mean(per)
     peak, peak_src = _peaks()
     achieved = b_hbm / (launch_ms * 1e-3) / 1e9
@@ -317,9 +330,11 @@ def main():
            "config": {"workload": cfg["name"], "k": k, "p": p, "d_p": cfg["d_p"], "n": n, "t": t,
                       "dist": "RSD" if cfg["dist"] == configs.RSD else "Omega",
                       "stripes_total": cfg["stripes"] * (ws if args.scaling == "weak" and kind == "stripes" else 1),
-                      "per_rank": ("%d stripes" % S) if kind == "stripes" else ("rows [%d,%d)" % (u0, u1)),
-                      "parallelism": ("stripe-sharded x%d" % ws) if kind == "stripes" else
-                                     ("coded-row partition x%d, source replicated" % ws),
+                      "per_rank": {"stripes": "%d stripes" % S, "rows": "rows [%d,%d)" % (u0, u1),
+                                   "cols": "bytes [%d,%d)" % (u0, u1)}[kind],
+                      "parallelism": {"stripes": "stripe-sharded x%d" % ws,
+                                      "rows": "coded-row partition x%d, source replicated" % ws,
+                                      "cols": "byte-column partition x%d, nothing replicated" % ws}[kind],
                       "variant": args.variant,
                       "l2": "inputs (%.2f GB per rank) exceed the 126 MB L2; no flush needed"
                             % (S * k * t / 1e9),

@@ -88,6 +88,9 @@ typedef struct {
   uint32_t fin_len;          /* FINITE: number of support points                             */
   uint64_t seed;          /* splitmix64 graph seed (reading R2/R3)                            */
   int32_t precode;        /* fs_precode_kind (0 = FS_PRECODE_RANDOM)                          */
+  uint32_t files;         /* s output files: 0 or 1 = one stream for all rows;
+                             s > 1 (s | n): rows [i n/s, (i+1) n/s) of file i drawn from a stream
+                             seeded seed + i (file 0 continues the base stream; reading R17)    */
 } fs_params;
 
 typedef struct fs_graph fs_graph;  /* opaque */
@@ -106,7 +109,7 @@ typedef struct fs_graph fs_graph;  /* opaque */
  * neighbour list sorted ascending (R14).  Without FS_GRAPH_HOST_ONLY the CSR and the work
  * schedules are uploaded to the current device (synchronously, before return).
  * FS_EINVAL: k == 0, n == 0, t == 0, t % 16 != 0 or t >= 2^31, p > 0 with d_p == 0 or d_p > k,
- *            K = k+p >= 2^31.
+ *            K = k+p >= 2^31, files > 1 not dividing n.
  * FS_EDIST:  empty support, degree 0, degrees not strictly increasing, negative weight,
  *            |sum - 1| > 1e-5, RSD c <= 0, delta outside (0,1), R/delta <= 1, K/R < 1.   */
 FSB_API fs_status fs_graph_create(const fs_params *prm, uint32_t flags, fs_graph **out);
@@ -156,6 +159,16 @@ FSB_API fs_status fs_graph_set_variant(fs_graph *g, int32_t variant);
  * Launches: GLOBAL = 1 precode kernel (if p > 0) + 1 LT kernel; SMEM = 1 fused kernel.   */
 FSB_API fs_status fs_encode(const fs_graph *g, const uint8_t *d_data, uint8_t *d_checks,
                     uint8_t *d_coded, uint32_t row_begin, uint32_t row_end, void *stream);
+
+/* fs_encode restricted to bytes [col_begin, col_end) of every symbol (byte-
+ * range partition of a single large stripe across GPUs -- each rank reads and writes only its
+ * columns, so unlike the row partition nothing is replicated).  Buffers are full-size as in
+ * fs_encode (symbol stride t); bytes outside the range are neither read nor written.  The p checks
+ * are computed for the range.  col_begin <= col_end <= t, multiples of 16, else FS_EINVAL.
+ * Takes the SMEM variant only for full row ranges on 64-B slice boundaries.                  */
+FSB_API fs_status fs_encode_range(const fs_graph *g, const uint8_t *d_data, uint8_t *d_checks,
+                                  uint8_t *d_coded, uint32_t row_begin, uint32_t row_end,
+                                  uint64_t col_begin, uint64_t col_end, void *stream);
 
 /* num_stripes stripes with the same graph.  Strides are in bytes and must be
  * multiples of 16 and >= k*t, p*t, n*t respectively.  0 stripes is a no-op.               */

@@ -187,7 +187,7 @@ int32_t or_array_precode(uint32_t k, uint32_t K, int32_t *pre_row_ptr, int32_t *
 int64_t or_generate_graph_ex(uint32_t k, uint32_t p, uint32_t d_p, uint32_t n, uint64_t seed,
                              int kind, double rsd_c, double rsd_delta,
                              const uint32_t *fin_deg, const double *fin_prob, uint32_t fin_len,
-                             int precode_kind,
+                             int precode_kind, uint32_t files,
                              int32_t *pre_row_ptr, int32_t *pre_col,
                              int32_t *lt_row_ptr, int32_t *lt_col);
 
@@ -196,16 +196,19 @@ int64_t or_generate_graph(uint32_t k, uint32_t p, uint32_t d_p, uint32_t n, uint
                           const uint32_t *fin_deg, const double *fin_prob, uint32_t fin_len,
                           int32_t *pre_row_ptr, int32_t *pre_col,
                           int32_t *lt_row_ptr, int32_t *lt_col) {
-  return or_generate_graph_ex(k, p, d_p, n, seed, kind, rsd_c, rsd_delta, fin_deg, fin_prob, fin_len, 0,
+  return or_generate_graph_ex(k, p, d_p, n, seed, kind, rsd_c, rsd_delta, fin_deg, fin_prob, fin_len, 0, 1,
                               pre_row_ptr, pre_col, lt_row_ptr, lt_col);
 }
 
 /* precode_kind 0: p random checks of d_p distinct data symbols drawn from the stream (R5, R11);
- * 1: Alg 2 array LDPC checks (deterministic, no stream draws; d_p is implied).            */
+ * 1: Alg 2 array LDPC checks (deterministic, no stream draws; d_p is implied).
+ * files = s output files: "the seed of the i-th output file" -- with
+ * s > 1 the n/s rows of file i >= 1 come from a fresh stream seeded seed + i, file 0 continues the
+ * base stream (reading R17); s <= 1 is the single stream.  s must divide n.               */
 int64_t or_generate_graph_ex(uint32_t k, uint32_t p, uint32_t d_p, uint32_t n, uint64_t seed,
                              int kind, double rsd_c, double rsd_delta,
                              const uint32_t *fin_deg, const double *fin_prob, uint32_t fin_len,
-                             int precode_kind,
+                             int precode_kind, uint32_t files,
                              int32_t *pre_row_ptr, int32_t *pre_col,
                              int32_t *lt_row_ptr, int32_t *lt_col) {
   uint32_t K = k + p, i, j, len;
@@ -215,6 +218,7 @@ int64_t or_generate_graph_ex(uint32_t k, uint32_t p, uint32_t d_p, uint32_t n, u
   double *cdf;
   int r;
   if (k == 0 || n == 0) return -1;
+  if (files > 1 && n % files != 0) return -1;
   if (precode_kind == 0 && p > 0 && (d_p == 0 || d_p > k)) return -1;
   if (precode_kind == 1 && (p == 0 || or_array_precode(k, K, pre_row_ptr, pre_col) < 0)) return -1;
   deg = (uint32_t *)malloc(sizeof(uint32_t) * (K + fin_len + 1));
@@ -233,7 +237,9 @@ int64_t or_generate_graph_ex(uint32_t k, uint32_t p, uint32_t d_p, uint32_t n, u
   /* step (2): LT rows: one degree draw, then the neighbour draws (R5, R12) */
   lt_row_ptr[0] = 0;
   for (j = 0; j < n; ++j) {
-    uint32_t d = draw_degree(&st, deg, cdf, len);
+    uint32_t d;
+    if (files > 1 && j > 0 && j % (n / files) == 0) st = seed + j / (n / files);  /* file i's stream */
+    d = draw_degree(&st, deg, cdf, len);
     if (d > K) d = K;
     draw_neighbours(&st, d, K, lt_col + nnz);
     nnz += d;

@@ -40,7 +40,7 @@ def lib():
                                         P, P, P, P]
         L.or_generate_graph.restype = i64
         L.or_generate_graph_ex.argtypes = [u32, u32, u32, u32, u64, ctypes.c_int, dbl, dbl, P, P, u32,
-                                           ctypes.c_int, P, P, P, P]
+                                           ctypes.c_int, u32, P, P, P, P]
         L.or_generate_graph_ex.restype = i64
         L.or_array_precode.argtypes = [u32, u32, P, P]
         L.or_array_precode.restype = ctypes.c_int32
@@ -109,7 +109,8 @@ def array_precode(k, K):
 
 
 def generate_graph(cfg):
-    """Graph generation a1 (readings R2-R15; NEXT-2: Alg 2 precode)."""
+    """Graph generation a1 (PAPER.md:91, 95, 103; readings R2-R15; NEXT-2: Alg 2 precode;
+    NEXT-4: cfg["files"] = s per-file streams seed + i, reading R17)."""
     k, p, n = cfg["k"], cfg["p"], cfg["n"]
     array = cfg.get("precode", "random") == "array"
     d_p = cfg["d_p"]
@@ -126,7 +127,7 @@ def generate_graph(cfg):
     lt_col = np.zeros(cap, dtype=np.int32)
     nnz = lib().or_generate_graph_ex(k, p, d_p, n, cfg["seed"], cfg["dist"], cfg.get("rsd_c", 0.0),
                                      cfg.get("rsd_delta", 0.0), _p(fd), _p(fp), len(fd), 1 if array else 0,
-                                     _p(pre_row_ptr), _p(pre_col), _p(lt_row_ptr), _p(lt_col))
+                                     int(cfg.get("files", 1)), _p(pre_row_ptr), _p(pre_col), _p(lt_row_ptr), _p(lt_col))
     if nnz < 0:
         raise ValueError("invalid graph parameters")
     return Graph(cfg, pre_row_ptr, pre_col[:p * d_p].copy(), lt_row_ptr, lt_col[:nnz].copy())

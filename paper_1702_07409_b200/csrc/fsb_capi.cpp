@@ -173,24 +173,36 @@ static fs_status check_device_graph(const fs_graph *h) {
   return FS_OK;
 }
 
-fs_status fs_encode(const fs_graph *h, const uint8_t *d_data, uint8_t *d_checks, uint8_t *d_coded,
-                    uint32_t row_begin, uint32_t row_end, void *stream) {
+fs_status fs_encode_range(const fs_graph *h, const uint8_t *d_data, uint8_t *d_checks, uint8_t *d_coded,
+                          uint32_t row_begin, uint32_t row_end, uint64_t col_begin, uint64_t col_end, void *stream) {
   fsb::set_error("");
   fsb::g_launches = 0;
   fs_status st = check_device_graph(h);
   if (st != FS_OK) return st;
   const fsb::Graph &g = h->g;
   if (row_begin > row_end || row_end > g.prm.n) { set_error("invalid row range"); return FS_EINVAL; }
+  if (col_begin > col_end || col_end > g.prm.t || col_begin % 16 || col_end % 16) {
+    set_error("invalid column range: need col_begin <= col_end <= t, multiples of 16");
+    return FS_EINVAL;
+  }
   if (!d_data || !aligned16(d_data)) { set_error("d_data must be a 16-B aligned device pointer"); return FS_EINVAL; }
   if (g.prm.p > 0 && (!d_checks || !aligned16(d_checks))) { set_error("d_checks must be 16-B aligned, non-NULL when p > 0"); return FS_EINVAL; }
   if (g.prm.p == 0 && d_checks) { set_error("d_checks must be NULL when p == 0"); return FS_EINVAL; }
   if (row_end > row_begin && (!d_coded || !aligned16(d_coded))) { set_error("d_coded must be a 16-B aligned device pointer"); return FS_EINVAL; }
+  if (col_end == col_begin) return FS_OK;
   const uint64_t t = g.prm.t;
   uint32_t launches = 0;
   st = fsb::launch_encode(g, 1, d_data, g.prm.k * t, d_checks, g.prm.p * t, d_coded,
-                          static_cast<uint64_t>(row_end - row_begin) * t, row_begin, row_end, stream, &launches);
+                          static_cast<uint64_t>(row_end - row_begin) * t, row_begin, row_end, col_begin, col_end,
+                          stream, &launches);
   if (st == FS_OK) fsb::g_launches = launches;
   return st;
+}
+
+fs_status fs_encode(const fs_graph *h, const uint8_t *d_data, uint8_t *d_checks, uint8_t *d_coded,
+                    uint32_t row_begin, uint32_t row_end, void *stream) {
+  if (!h) { fsb::set_error("null graph"); fsb::g_launches = 0; return FS_EINVAL; }
+  return fs_encode_range(h, d_data, d_checks, d_coded, row_begin, row_end, 0, h->g.prm.t, stream);
 }
 
 fs_status fs_encode_stripes(const fs_graph *h, uint32_t S, const uint8_t *d_data, uint64_t data_stride,
@@ -217,8 +229,8 @@ fs_status fs_encode_stripes(const fs_graph *h, uint32_t S, const uint8_t *d_data
     return FS_EINVAL;
   }
   uint32_t launches = 0;
-  st = fsb::launch_encode(g, S, d_data, data_stride, d_checks, checks_stride, d_coded, coded_stride, 0, g.prm.n,
-                          stream, &launches);
+  st = fsb::launch_encode(g, S, d_data, data_stride, d_checks, checks_stride, d_coded, coded_stride, 0, g.prm.n, 0,
+                          g.prm.t, stream, &launches);
   if (st == FS_OK) fsb::g_launches = launches;
   return st;
 }

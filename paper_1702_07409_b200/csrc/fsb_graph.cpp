@@ -14,6 +14,7 @@
 #include <queue>
 #include <cstdlib>
 #include <string>
+#include <thread>
 
 #include "fsb_internal.h"
 
@@ -98,6 +99,10 @@ fs_status validate_params(const fs_params &prm) {
     return FS_EINVAL;
   }
   if (static_cast<uint64_t>(prm.k) + prm.p >= (1ull << 31)) { set_error("k+p too large"); return FS_EINVAL; }
+  if (prm.files > 1 && prm.n % prm.files != 0) {
+    set_error("per-file streams need files | n (PAPER.md:88)");
+    return FS_EINVAL;
+  }
   if (prm.dist != FS_DIST_RSD && prm.dist != FS_DIST_FINITE) { set_error("unknown distribution"); return FS_EDIST; }
   return FS_OK;
 }
@@ -200,24 +205,62 @@ fs_status generate_csr(Graph &g) {
       g.pre_row_ptr[i + 1] = static_cast<int32_t>((i + 1) * prm.d_p);
     }
   }
-  // step (2): LT rows, one degree draw then the neighbour draws (R5, R12)
+  // step (2): LT rows, one degree draw then the neighbour draws (R5, R12).  With s = files > 1
+  // output file i (rows [i n/s, (i+1) n/s)) draws from its own stream seeded seed + i
+  // (reading R17); file 0 continues the base stream after the precode draws, so
+  // s = 1 is the single stream.  Files are independent: generated on parallel host threads.
+  const uint32_t s = std::max<uint32_t>(prm.files, 1), rows_per = n / s;
+  struct FileRows {
+    std::vector<int32_t> col, len;
+    uint32_t max_degree = 0;
+  };
+  std::vector<FileRows> files(s);
+  auto gen_file = [&](uint32_t f, SplitMix64 frng, NeighbourSampler &smp) {
+    FileRows &fr = files[f];
+    fr.len.resize(rows_per);
+    fr.col.reserve(static_cast<size_t>(rows_per) * 8);
+    std::vector<int32_t> row;
+    for (uint32_t j = 0; j < rows_per; ++j) {
+      const uint64_t x = frng.next();
+      const double u = static_cast<double>(x >> 11) * 0x1.0p-53;
+      const size_t idx = static_cast<size_t>(std::upper_bound(cdf.begin(), cdf.end(), u) - cdf.begin());
+      uint32_t d = deg[std::min(idx, deg.size() - 1)];
+      if (d > K) d = K;
+      row.resize(d);
+      smp.draw(frng, d, K, row.data());
+      fr.col.insert(fr.col.end(), row.begin(), row.end());
+      fr.len[j] = static_cast<int32_t>(d);
+      fr.max_degree = std::max(fr.max_degree, d);
+    }
+  };
+  if (s == 1) {
+    gen_file(0, rng, sampler);
+  } else {
+    const uint32_t hw = std::max(1u, std::min(std::thread::hardware_concurrency(), 32u));
+    const uint32_t nthreads = std::min(s, hw);
+    std::vector<std::thread> pool;
+    for (uint32_t w = 0; w < nthreads; ++w)
+      pool.emplace_back([&, w] {
+        NeighbourSampler smp(K);
+        for (uint32_t f = w; f < s; f += nthreads) gen_file(f, f == 0 ? rng : SplitMix64(prm.seed + f), smp);
+      });
+    for (auto &th : pool) th.join();
+  }
   g.lt_row_ptr.assign(n + 1, 0);
   g.lt_col.clear();
-  g.lt_col.reserve(static_cast<size_t>(n) * 8);
   g.max_degree = 0;
-  std::vector<int32_t> row;
-  for (uint32_t j = 0; j < n; ++j) {
-    const uint64_t x = rng.next();
-    const double u = static_cast<double>(x >> 11) * 0x1.0p-53;
-    const size_t idx = static_cast<size_t>(std::upper_bound(cdf.begin(), cdf.end(), u) - cdf.begin());
-    uint32_t d = deg[std::min(idx, deg.size() - 1)];
-    if (d > K) d = K;
-    row.resize(d);
-    sampler.draw(rng, d, K, row.data());
-    g.lt_col.insert(g.lt_col.end(), row.begin(), row.end());
-    if (g.lt_col.size() >= (1ull << 31)) { set_error("graph too large (nnz >= 2^31)"); return FS_EINVAL; }
-    g.lt_row_ptr[j + 1] = static_cast<int32_t>(g.lt_col.size());
-    g.max_degree = std::max(g.max_degree, d);
+  size_t nnz = 0;
+  for (const FileRows &fr : files) nnz += fr.col.size();
+  if (nnz >= (1ull << 31)) { set_error("graph too large (nnz >= 2^31)"); return FS_EINVAL; }
+  g.lt_col.reserve(nnz);
+  uint32_t j = 0;
+  for (const FileRows &fr : files) {
+    g.lt_col.insert(g.lt_col.end(), fr.col.begin(), fr.col.end());
+    for (int32_t d : fr.len) {
+      g.lt_row_ptr[j + 1] = g.lt_row_ptr[j] + d;
+      ++j;
+    }
+    g.max_degree = std::max(g.max_degree, fr.max_degree);
   }
   return FS_OK;
 }

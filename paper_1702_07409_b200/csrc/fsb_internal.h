@@ -111,8 +111,8 @@ fs_status upload_graph(Graph &g);
 void free_device(Graph &g);
 fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_t data_stride,
                         uint8_t *checks, uint64_t checks_stride, uint8_t *coded,
-                        uint64_t coded_stride, uint32_t row_begin, uint32_t row_end, void *stream,
-                        uint32_t *launches);
+                        uint64_t coded_stride, uint32_t row_begin, uint32_t row_end, uint64_t col_begin,
+                        uint64_t col_end, void *stream, uint32_t *launches);
 
 fs_status read_debug_counters(uint64_t *out, uint32_t n);
 

@@ -119,6 +119,7 @@ struct SmemArgs {
   uint64_t coded_stride;
   uint64_t t;
   uint32_t nslices, ntiles, p, d_p, kpad, zero_even, data_units, tile_units;
+  uint32_t slice0;             // first 64-B slice of the column range
   uint32_t sched_chunks, cont_base;
   uint32_t debug;              // FSB_DEBUG bits (profiling experiments only; 0 in production)
   uint32_t wait_ns;            // consumer sleep between probes of a tile's `ready` barrier
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t i = 0;
       for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
         const uint32_t b = i & 1, ph = (i >> 1) & 1;
-        const uint32_t stripe = tile / a.nslices, slice = tile % a.nslices;
+        const uint32_t stripe = tile / a.nslices, slice = a.slice0 + tile % a.nslices;
         const uint32_t buf = smem_base + b * buf_bytes;
         mbar_wait(smem_u32(&empty[b]), ph ^ 1);  // consumers released tile i-2
         if (a.debug & 1) {  // experiment: no TMA (consumers gather stale rows)
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t i = 0;
     for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
       const uint32_t b = i & 1, ph = (i >> 1) & 1;
-      const uint32_t stripe = tile / a.nslices, slice = tile % a.nslices;
+      const uint32_t stripe = tile / a.nslices, slice = a.slice0 + tile % a.nslices;
       const uint32_t buf = smem_base + b * buf_bytes;
       mbar_wait(smem_u32(&full[b]), ph);
       // precode, level by level (a check may read checks of earlier levels, Alg 2): check c of
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const long long t_start = (a.debug & 2) ? clock64() : 0;
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
     const uint32_t b = i & 1, ph = (i >> 1) & 1;
-    const uint32_t stripe = tile / a.nslices, slice = tile % a.nslices;
+    const uint32_t stripe = tile / a.nslices, slice = a.slice0 + tile % a.nslices;
     const uint32_t sbase = smem_base + b * buf_bytes + lane4 * 16;  // this lane's 16 B of tile row 0
     uint32_t hp = head0, cp = cont0;
     uint4 h0 = lds128(hp);
@@ -369,8 +370,8 @@ constexpr uint32_t kGSliceBytes = 128;  // one 8-lane group = 8 x 16 B
 // Checks [c0, c0 + nc) of one precode level: one 8-lane group per (stripe, check, 128-B slice).
 // A member m >= k is a check of an earlier level (Alg 2), read from the checks buffer.
 __global__ void __launch_bounds__(kGlobalThreads)
-    fsb_precode_global(uint32_t S, uint32_t c0, uint32_t nc, uint32_t k, uint32_t d_p, uint64_t t,
-                       uint32_t nslices, const int32_t *__restrict__ pre_col, const uint8_t *__restrict__ data,
+    fsb_precode_global(uint32_t S, uint32_t c0, uint32_t nc, uint32_t k, uint32_t d_p, uint64_t t, uint64_t col0,
+                       uint64_t col1, uint32_t nslices, const int32_t *__restrict__ pre_col, const uint8_t *__restrict__ data,
                        uint64_t data_stride, uint8_t *checks, uint64_t checks_stride) {
   const uint64_t item = static_cast<uint64_t>(blockIdx.x) * kGroupsPerBlock + (threadIdx.x >> 3);
   const uint32_t lane8 = threadIdx.x & 7;
@@ -380,8 +381,8 @@ __global__ void __launch_bounds__(kGlobalThreads)
   const uint64_t r = item / nslices;
   const uint32_t c = c0 + static_cast<uint32_t>(r % nc);
   const uint32_t s = static_cast<uint32_t>(r / nc);
-  const uint64_t byte = static_cast<uint64_t>(slice) * kGSliceBytes + lane8 * 16;
-  if (byte >= t) return;
+  const uint64_t byte = col0 + static_cast<uint64_t>(slice) * kGSliceBytes + lane8 * 16;
+  if (byte >= col1) return;
   const uint8_t *src = data + s * data_stride + byte;
   const uint8_t *csrc = checks + s * checks_stride + byte;
   uint4 acc = make_uint4(0, 0, 0, 0);
@@ -407,8 +408,8 @@ constexpr uint32_t kBandRowsMax = 8;   // coded rows per warp (fewer when the ca
 
 template <uint32_t kBandBatch, int kMinBlocks>
 __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
-    fsb_lt_band(uint32_t S, uint32_t k, uint32_t t, uint32_t nbands, uint32_t row_begin, uint32_t nrows,
-                uint32_t band_rows, const int32_t *__restrict__ row_ptr, const uint32_t *__restrict__ colf,
+    fsb_lt_band(uint32_t S, uint32_t k, uint32_t t, uint32_t col0, uint32_t col1, uint32_t nbands, uint32_t row_begin,
+                uint32_t nrows, uint32_t band_rows, const int32_t *__restrict__ row_ptr, const uint32_t *__restrict__ colf,
                 const uint8_t *__restrict__ data, uint64_t data_stride, const uint8_t *__restrict__ checks,
                 uint64_t checks_stride, uint8_t *__restrict__ coded, uint64_t coded_stride) {
   const uint32_t lane = threadIdx.x & 31;
@@ -419,9 +420,9 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   const uint32_t band = static_cast<uint32_t>(unit % nbands);
   const uint64_t s = unit / nbands;
   if (s >= S) return;
-  const uint32_t byte_raw = band * kBandBytes + lane * 16;
-  const bool active = byte_raw < t;                   // ragged last band
-  const uint32_t byte = active ? byte_raw : 0;        // inactive lanes load a valid address
+  const uint32_t byte_raw = col0 + band * kBandBytes + lane * 16;  // bands cover columns [col0, col1)
+  const bool active = byte_raw < col1;                // ragged last band
+  const uint32_t byte = active ? byte_raw : col0;     // inactive lanes load a valid address
   // source row m lives at (m < k ? dbase : cbase) + m*t  (checks: row k+i = check i)
   const uint8_t *dbase = data + s * data_stride + byte;
   const uint8_t *cbase = checks + s * checks_stride + byte - static_cast<uint64_t>(k) * t;
@@ -620,12 +621,15 @@ fs_status upload_graph(Graph &g) {
 
 fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_t data_stride, uint8_t *checks,
                         uint64_t checks_stride, uint8_t *coded, uint64_t coded_stride, uint32_t row_begin,
-                        uint32_t row_end, void *stream_ptr, uint32_t *launches) {
+                        uint32_t row_end, uint64_t col_begin, uint64_t col_end, void *stream_ptr, uint32_t *launches) {
   *launches = 0;
   const fs_params &prm = g.prm;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
-  const uint32_t nslices = static_cast<uint32_t>((prm.t + kSliceBytes - 1) / kSliceBytes);
-  const bool full_rows = row_begin == 0 && row_end == prm.n;
+  // SMEM tiles need the column range on 64-B slice boundaries
+  const bool slice_aligned = col_begin % kSliceBytes == 0 && (col_end % kSliceBytes == 0 || col_end == prm.t);
+  const uint32_t slice0 = static_cast<uint32_t>(col_begin / kSliceBytes);
+  const uint32_t nslices = static_cast<uint32_t>((col_end + kSliceBytes - 1) / kSliceBytes) - slice0;
+  const bool full_rows = row_begin == 0 && row_end == prm.n && slice_aligned;
   const uint64_t tiles = static_cast<uint64_t>(S) * nslices;
   bool use_smem = false;
   if (g.variant == FS_VARIANT_SMEM) {
@@ -665,6 +669,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     a.coded_stride = coded_stride;
     a.t = prm.t;
     a.nslices = nslices;
+    a.slice0 = slice0;
     a.ntiles = static_cast<uint32_t>(tiles);
     a.p = prm.p;
     a.d_p = prm.d_p;
@@ -692,19 +697,20 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     *launches = 1;
     return FS_OK;
   }
-  const uint32_t gslices = static_cast<uint32_t>((prm.t + kGSliceBytes - 1) / kGSliceBytes);
+  const uint32_t gslices = static_cast<uint32_t>((col_end - col_begin + kGSliceBytes - 1) / kGSliceBytes);
   for (size_t L = 0; prm.p && L + 1 < g.pre_level_ptr.size(); ++L) {  // one launch per precode level
     const uint32_t c0 = g.pre_level_ptr[L], nc = g.pre_level_ptr[L + 1] - c0;
     const uint64_t items = static_cast<uint64_t>(S) * nc * gslices;
     const uint64_t blocks = (items + kGroupsPerBlock - 1) / kGroupsPerBlock;
     fsb_precode_global<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, c0, nc, prm.k, prm.d_p, prm.t, gslices, g.dev.pre_col, data, data_stride, checks, checks_stride);
+        S, c0, nc, prm.k, prm.d_p, prm.t, col_begin, col_end, gslices, g.dev.pre_col, data, data_stride, checks,
+        checks_stride);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_precode_global launch");
     ++*launches;
   }
   const uint32_t nrows = row_end - row_begin;
   if (nrows) {
-    const uint32_t nbands = static_cast<uint32_t>((prm.t + kBandBytes - 1) / kBandBytes);
+    const uint32_t nbands = static_cast<uint32_t>((col_end - col_begin + kBandBytes - 1) / kBandBytes);
     // rows per warp: up to kBandRowsMax, fewer if that leaves fewer than ~64 warps per SM
     const uint64_t row_bands = static_cast<uint64_t>(S) * nbands * nrows;
     const uint32_t band_rows = static_cast<uint32_t>(
@@ -723,7 +729,8 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     if (band_cfg == 0) kern = fsb_lt_band<4, 6>;
     if (band_cfg == 2) kern = fsb_lt_band<8, 4>;
     kern<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, prm.k, static_cast<uint32_t>(prm.t), nbands, row_begin, nrows, band_rows, g.dev.lt_row_ptr,
+        S, prm.k, static_cast<uint32_t>(prm.t), static_cast<uint32_t>(col_begin), static_cast<uint32_t>(col_end),
+        nbands, row_begin, nrows, band_rows, g.dev.lt_row_ptr,
         g.dev.lt_colf, data, data_stride, checks, checks_stride, coded, coded_stride);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_lt_band launch");
     ++*launches;

@@ -1,8 +1,9 @@
 """Multi-GPU plumbing of the encode path -- host logic only.
 
 One process per GPU.  The units of work are independent: stripes ("partitions are
-processed independent of each other") for multi-stripe encodes, or coded-row ranges of one stripe
-(reading R16) for a single large stripe.  The only collective is step a2: rank 0 generates the
+processed independent of each other") for multi-stripe encodes, or, for a single large stripe,
+coded-row ranges (reading R16) or byte-column ranges (every symbol XOR is bytewise, so columns are
+independent; fs_encode_range).  The only collective is step a2: rank 0 generates the
 graph (fs_graph_create) and broadcasts its CSR; the other ranks rebuild it with
 fs_graph_from_csr.  There is no data-path collective.
 
@@ -20,6 +21,16 @@ def shard(total, world_size, rank):
     if world_size < 1 or not 0 <= rank < world_size:
         raise ValueError("bad world_size / rank")
     return rank * total // world_size, (rank + 1) * total // world_size
+
+
+def col_shard(t, world_size, rank, align=64):
+    """Contiguous byte range [c0, c1) of a t-byte symbol for `rank` (NEXT-4 column partition):
+    boundaries on `align`-byte multiples (64 = one SMEM slice) except the final end t."""
+    if t % 16:
+        raise ValueError("t must be a multiple of 16")
+    units = (t + align - 1) // align
+    a, b = shard(units, world_size, rank)
+    return min(a * align, t), min(b * align, t)
 
 
 def broadcast_graph(cfg, group=None, device="cpu", host_only=False):

@@ -23,7 +23,7 @@ EXPORTS = ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get
            "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_last_launch_count",
            "fs_free", "fs_last_error", "fs_version", "fs_graph_schedule", "fs_debug_counters",
            "fs_decode_plan_create", "fs_decode_plan_info", "fs_decode_plan_state", "fs_decode",
-           "fs_decode_plan_free")
+           "fs_decode_plan_free", "fs_encode_range")
 
 
 class FsError(RuntimeError):
@@ -38,7 +38,7 @@ class fs_params(ctypes.Structure):
                 ("rsd_c", ctypes.c_double), ("rsd_delta", ctypes.c_double),
                 ("fin_deg", ctypes.POINTER(ctypes.c_uint32)),
                 ("fin_prob", ctypes.POINTER(ctypes.c_double)), ("fin_len", ctypes.c_uint32),
-                ("seed", ctypes.c_uint64), ("precode", ctypes.c_int32)]
+                ("seed", ctypes.c_uint64), ("precode", ctypes.c_int32), ("files", ctypes.c_uint32)]
 
 
 class fs_graph_info(ctypes.Structure):
@@ -76,6 +76,8 @@ def lib():
         L.fs_graph_get_info.argtypes = [P, ctypes.POINTER(fs_graph_info)]
         L.fs_graph_set_variant.argtypes = [P, i32]
         L.fs_encode.argtypes = [P, P, P, P, u32, u32, P]
+        L.fs_encode_range.argtypes = [P, P, P, P, u32, u32, u64, u64, P]
+        L.fs_encode_range.restype = ctypes.c_int
         L.fs_encode_stripes.argtypes = [P, u32, P, u64, P, u64, P, u64, P]
         L.fs_graph_schedule.argtypes = [P, PP, ctypes.POINTER(u64), ctypes.POINTER(u32), PP,
                                         ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u32)]
@@ -144,6 +146,7 @@ def make_params(cfg):
     prm.fin_len = len(fd)
     prm.seed = cfg["seed"]
     prm.precode = {"random": FS_PRECODE_RANDOM, "array": FS_PRECODE_ARRAY}[cfg.get("precode", "random")]
+    prm.files = int(cfg.get("files", 1))
     return prm
 
 
@@ -222,6 +225,11 @@ class Graph:
         row_end = self.n if row_end is None else row_end
         _check(lib().fs_encode(self._h, _ptr(data), _ptr(checks), _ptr(coded), row_begin, row_end,
                                _stream(stream)))
+
+    def encode_range(self, data, checks, coded, row_begin, row_end, col_begin, col_end, stream=None):
+        """fs_encode_range: rows [row_begin, row_end) and bytes [col_begin, col_end) of one stripe."""
+        _check(lib().fs_encode_range(self._h, _ptr(data), _ptr(checks), _ptr(coded), row_begin, row_end,
+                                     col_begin, col_end, _stream(stream)))
 
     def encode_stripes(self, data, checks, coded, stream=None):
         """fs_encode_stripes over contiguous [S,k,t] / [S,p,t] / [S,n,t] uint8 CUDA tensors."""

@@ -273,3 +273,23 @@ def test_array_precode_validation():
     bad[0] = c["k"] + 5                                  # check 0 reading check 5
     with pytest.raises(fsb.FsError):
         fsb.Graph.from_csr(c, pre_rp, bad, lt_rp, lt_c, host_only=True)
+
+
+@pytest.mark.parametrize("cid,files", [(1, 13), (2, 10), (4, 8), (5, 12), (6, 4), (3, 1)])
+def test_per_file_streams_library_matches_oracle(cid, files):
+    """NEXT-4 / R17: per-file seed streams seed + i, library (threaded) == oracle."""
+    c = dict(configs.get(cid), files=files)
+    g = fsb.Graph.create(c, host_only=True)
+    o = oracle.generate_graph(c)
+    a = g.csr()
+    for x, y in zip(a, (o.pre_row_ptr, o.pre_col, o.lt_row_ptr, o.lt_col)):
+        assert np.array_equal(x, y)
+    assert g.info()["max_degree"] == int(np.diff(o.lt_row_ptr).max())
+
+
+def test_per_file_streams_reject_non_divisor():
+    c = dict(configs.get(1), files=7)          # 7 does not divide n = 130
+    with pytest.raises(fsb.FsError):
+        fsb.Graph.create(c, host_only=True)
+    with pytest.raises(ValueError):
+        oracle.generate_graph(c)

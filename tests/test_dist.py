@@ -94,3 +94,23 @@ def test_bench_plan():
             assert all(k == "rows" for k, _, _ in rows)
             assert rows[0][1] == 0 and rows[-1][2] == c5["n"]
             assert all(rows[i][2] == rows[i + 1][1] for i in range(ws - 1))
+
+
+def test_col_shard_covers_exactly_once():
+    for t in (16, 64, 80, 4096, 320 * 1024, 1000016):
+        for ws in (1, 2, 3, 4, 8):
+            parts = [fdist.col_shard(t, ws, r) for r in range(ws)]
+            assert parts[0][0] == 0 and parts[-1][1] == t
+            for (a, b), (c, d) in zip(parts, parts[1:]):
+                assert b == c
+            for a, b in parts:
+                assert a <= b and a % 64 == 0 and (b % 64 == 0 or b == t)
+
+
+def test_bench_plan_cols():
+    import bench
+    c5 = configs.get(5)
+    for ws in (2, 4, 8):
+        parts = [bench.plan(c5, ws, r, "strong", "cols") for r in range(ws)]
+        assert all(k == "cols" for k, _, _ in parts)
+        assert parts[0][1] == 0 and parts[-1][2] == c5["t"]

@@ -91,6 +91,45 @@ def test_row_range_partition_concatenates():
         _assert_equal(torch.cat(parts).cpu().numpy(), Y[0], "row partition G=%d" % G)
 
 
+@pytest.mark.parametrize("cid,variant", [(5, fsb.VARIANT_AUTO), (3, fsb.VARIANT_GLOBAL),
+                                         (4, fsb.VARIANT_SMEM), (4, fsb.VARIANT_GLOBAL)])
+def test_col_range_partition_concatenates(cid, variant):
+    """NEXT-4: fs_encode_range over byte columns [c0, c1) per rank assembles the full output;
+    bytes outside a rank's columns are untouched; 16-B (non-slice) boundaries take GLOBAL."""
+    _need_gpu()
+    from paper_1702_07409_b200 import dist as fdist
+    cfg = dict(configs.get(cid))
+    cfg["stripes"] = 1
+    g = fsb.Graph.create(cfg)
+    g.set_variant(variant)
+    D, C, Y = _oracle_case(cfg)
+    d = torch.from_numpy(D[0]).cuda()
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    splits = [[fdist.col_shard(t, G, r) for r in range(G)] for G in (2, 3, 8)]
+    splits.append([(0, 16), (16, t - 48), (t - 48, t)])          # 16-B boundaries
+    for parts in splits:
+        chk = torch.full((p, t), 0xA5, dtype=torch.uint8, device="cuda") if p else None
+        out = torch.full((n, t), 0x5A, dtype=torch.uint8, device="cuda")
+        for c0, c1 in parts:
+            g.encode_range(d, chk, out, 0, n, c0, c1)
+            torch.cuda.synchronize()
+            o = out.cpu().numpy()
+            _assert_equal(o[:, c0:c1], Y[0][:, c0:c1], "coded cols [%d,%d)" % (c0, c1))
+            assert (o[:, c1:] == 0x5A).all(), "wrote past col_end"
+            if p:
+                _assert_equal(chk.cpu().numpy()[:, c0:c1], C[0][:, c0:c1], "checks cols [%d,%d)" % (c0, c1))
+        _assert_equal(out.cpu().numpy(), Y[0], "column partition %s" % (parts[:2],))
+    # a rows x cols sub-block (row range goes GLOBAL)
+    a, b, c0, c1 = n // 3, n // 2, 64 * 5, t - 64
+    out = torch.full((b - a, t), 0x5A, dtype=torch.uint8, device="cuda")
+    chk = torch.empty((p, t), dtype=torch.uint8, device="cuda") if p else None
+    g.encode_range(d, chk, out, a, b, c0, c1)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    _assert_equal(o[:, c0:c1], Y[0][a:b, c0:c1], "rows x cols block")
+    assert (o[:, :c0] == 0x5A).all() and (o[:, c1:] == 0x5A).all()
+
+
 def test_stripes_equal_single_encodes():
     """P10: fs_encode_stripes over S stripes = S independent fs_encode calls."""
     _need_gpu()
@@ -187,6 +226,21 @@ def test_empty_calls_are_noops():
     g.encode_stripes(d[:0], None, torch.empty((0, cfg["n"], cfg["t"]), dtype=torch.uint8, device="cuda"))
     torch.cuda.synchronize()
     assert torch.all(out == 7)
+
+
+def test_invalid_arguments_rejected_range():
+    _need_gpu()
+    cfg = configs.get(1)
+    g = fsb.Graph.create(cfg)
+    t, n = cfg["t"], cfg["n"]
+    d = inputs.stripe_data(cfg, device="cuda")[0]
+    chk = torch.empty((cfg["p"], t), dtype=torch.uint8, device="cuda")
+    out = torch.empty((n, t), dtype=torch.uint8, device="cuda")
+    for c0, c1 in ((8, 64), (0, 24 + 1), (64, 32), (0, t + 16)):
+        with pytest.raises(fsb.FsError):
+            g.encode_range(d, chk, out, 0, n, c0, c1)
+    g.encode_range(d, chk, out, 0, n, 32, 32)                        # empty range: no-op
+    assert fsb.last_launch_count() == 0
 
 
 def test_invalid_arguments_rejected():
