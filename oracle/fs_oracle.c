@@ -467,3 +467,61 @@ int64_t or_decode(uint32_t k, uint32_t p, uint32_t n, uint64_t t,
   free(chk);
   return recovered;
 }
+
+/* ------------------------------------------------- CGA, Algorithm 4 (NEXT-3, repair/update)
+ * Check Generation Algorithm, written out step by step on dense 0/1
+ * matrices.  B in F2^{K x n}: column j = the neighbours of coded symbol j (the generator matrix
+ * of the base code; the paper's k = our K = k+p intermediate symbols,
+ * reading R19).  L^{(2,3)} starts as I_n.  Column-major storage:
+ * B[j*K + x], L[j*n + s].
+ *   while zero_columns(B) < n - K:              (R19: the test counts ZERO columns)
+ *     temp = 0
+ *     for j in 0..n-1: for i in 0..n-1:
+ *       if j != i and 2 w(b_j) > w(b_i):
+ *         if w(b_j XOR b_i) < w(b_j): b_j ^= b_i; l_j ^= l_i; temp = 1
+ *     if temp == 0: break
+ * Returns the number of executed sweeps (passes of the while body).                        */
+static uint32_t col_weight(const uint8_t *c, uint32_t len) {
+  uint32_t x, w = 0;
+  for (x = 0; x < len; ++x) w += c[x];
+  return w;
+}
+
+int32_t or_cga(uint32_t K, uint32_t n, const int32_t *lt_row_ptr, const int32_t *lt_col,
+               uint8_t *B, uint8_t *L) {
+  uint32_t i, j, x;
+  int32_t e, sweeps = 0;
+  memset(B, 0, (size_t)K * n);
+  memset(L, 0, (size_t)n * n);
+  for (j = 0; j < n; ++j) {
+    for (e = lt_row_ptr[j]; e < lt_row_ptr[j + 1]; ++e) B[(size_t)j * K + (uint32_t)lt_col[e]] = 1;
+    L[(size_t)j * n + j] = 1;
+  }
+  for (;;) {
+    uint32_t zero = 0;
+    int temp = 0;
+    for (j = 0; j < n; ++j) zero += col_weight(B + (size_t)j * K, K) == 0;
+    if (!((int64_t)zero < (int64_t)n - (int64_t)K)) break;
+    ++sweeps;
+    for (j = 0; j < n; ++j) {
+      uint8_t *bj = B + (size_t)j * K;
+      for (i = 0; i < n; ++i) {
+        const uint8_t *bi = B + (size_t)i * K;
+        uint32_t wj, wx = 0;
+        if (i == j) continue;
+        wj = col_weight(bj, K);
+        if (!(2 * wj > col_weight(bi, K))) continue;
+        for (x = 0; x < K; ++x) wx += bj[x] ^ bi[x];
+        if (wx < wj) {
+          uint8_t *lj = L + (size_t)j * n;
+          const uint8_t *li = L + (size_t)i * n;
+          for (x = 0; x < K; ++x) bj[x] ^= bi[x];
+          for (x = 0; x < n; ++x) lj[x] ^= li[x];
+          temp = 1;
+        }
+      }
+    }
+    if (!temp) break;
+  }
+  return sweeps;
+}

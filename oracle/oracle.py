@@ -50,6 +50,8 @@ def lib():
         L.or_encode_stripes.restype = None
         L.or_decode.argtypes = [u32, u32, u32, u64, P, P, P, P, P, P, ctypes.c_int, P, P]
         L.or_decode.restype = i64
+        L.or_cga.argtypes = [u32, u32, P, P, P, P]
+        L.or_cga.restype = ctypes.c_int32
         _lib = L
     return _lib
 
@@ -164,3 +166,181 @@ def decode(g, recv_mask, coded, use_elim=True):
     if r < 0:
         raise MemoryError("oracle decode failed")
     return out, state
+
+
+# ------------------------------------------------------------------ NEXT-3: repair and update
+def cga(g):
+    """Algorithm 4 (CGA) on B = the LT generator (K x n).  Returns the final
+    B (K x n, 0/1), L^{(2,3)} (n x n: column j = the coded symbols of local set j) and the number
+    of sweeps.  Dense and slow: small graphs only."""
+    K, n = g.K, g.n
+    Bt = np.zeros((n, K), dtype=np.uint8)          # column-major: row j of Bt = column j of B
+    Lt = np.zeros((n, n), dtype=np.uint8)
+    sweeps = lib().or_cga(K, n, _p(g.lt_row_ptr), _p(g.lt_col), _p(Bt), _p(Lt))
+    return Bt.T.copy(), Lt.T.copy(), int(sweeps)
+
+
+CHECKS_M1 = 1      # PAPER.md:247, first method: degree-one coded nodes
+CHECKS_M2 = 2      # PAPER.md:248-260, second method: check #1 groups via setXOR (Eq 4)
+
+
+def local_groups(g, B, L):
+    """The local recovery sets of PAPER.md:266-268 from CGA's output: column j of B with weight 0
+    -> Group #3 {C_s : l_{s,j} = 1}; weight 1 (symbol x) -> Group #2 (x, {C_s : l_{s,j} = 1});
+    weight >= 2 -> no group.  Returns [(kind, x or -1, sorted members, order key j)]."""
+    out = []
+    for j in range(g.n):
+        w = int(B[:, j].sum())
+        members = [int(s) for s in np.nonzero(L[:, j])[0]]
+        if w == 0:
+            out.append((3, -1, members, j))
+        elif w == 1:
+            out.append((2, int(np.nonzero(B[:, j])[0][0]), members, j))
+    return out
+
+
+def set_xor(*sets):
+    """setXOR: symmetric difference of index sets."""
+    acc = set()
+    for s in sets:
+        acc ^= set(s)
+    return acc
+
+
+def derived_groups(g, groups, flags):
+    """Extra Group #3 sets.  G_x = the first Group #2 set of symbol x in
+    (cardinality, j) order (reading R20).  Method 1: coded node j of degree one
+    with neighbour x gives G_x XOR {j}.  Method 2: a check #1 group (members
+    of precode check i and the check symbol k+i) whose symbols all have a G_x gives
+    setXOR of those G_x (Eq 4).  Empty results are dropped.  Order keys n, n+1, ..."""
+    g2 = {}
+    for kind, x, mem, j in sorted(groups, key=lambda t: (len(t[2]), t[3])):
+        if kind == 2 and x not in g2:
+            g2[x] = mem
+    out = []
+    if flags & CHECKS_M1:
+        for j in range(g.n):
+            row = list(g.lt_row(j))
+            if len(row) == 1 and row[0] in g2:
+                d = set_xor(g2[row[0]], [j])
+                if d:
+                    out.append(d)
+    if flags & CHECKS_M2:
+        for i in range(g.p):
+            grp = [int(m) for m in g.pre_row(i)] + [g.k + i]
+            if all(x in g2 for x in grp):
+                d = set_xor(*[g2[x] for x in grp])
+                if d:
+                    out.append(d)
+    return [(3, -1, sorted(d), g.n + m) for m, d in enumerate(out)]
+
+
+def check_data(g, flags=0):
+    """The <filename>_check.data integer array: per local set, Group #3 as
+    [0, deg, members...], Group #2 as [1, x, deg, members...]; sets ordered by cardinality
+    (smallest first), ties by order key (reading R20).  Returns (int32 array,
+    number of CGA sweeps)."""
+    B, L, sweeps = cga(g)
+    groups = local_groups(g, B, L)
+    groups = groups + derived_groups(g, groups, flags)
+    arr = []
+    for kind, x, mem, _ in sorted(groups, key=lambda t: (len(t[2]), t[3])):
+        arr += ([0, len(mem)] if kind == 3 else [1, x, len(mem)]) + mem
+    return np.array(arr, dtype=np.int32), sweeps
+
+
+def parse_check_data(arr):
+    """Inverse of the format: [(kind, x or -1, members)]."""
+    out, i, a = [], 0, [int(v) for v in arr]
+    while i < len(a):
+        if a[i] == 0:
+            d = a[i + 1]
+            out.append((3, -1, a[i + 2:i + 2 + d]))
+            i += 2 + d
+        elif a[i] == 1:
+            x, d = a[i + 1], a[i + 2]
+            out.append((2, x, a[i + 3:i + 3 + d]))
+            i += 3 + d
+        else:
+            raise ValueError("bad check data flag %d at %d" % (a[i], i))
+    return out
+
+
+def repair_plan(g, arr, erased, want=()):
+    """Repair / update / degraded read (reading R21).
+    Unknowns: the erased coded symbols (and, for a degraded read, the wanted intermediate
+    symbols; the data is not stored).  Local sets from the check data, in array order:
+      A  Group #3 set with exactly one unknown member x: x = XOR of the other members
+         (PAPER.md:336 "sequentially searches only one unknown over the available local sets").
+      B  unknown coded symbol j, ascending: if every neighbour x of j (the base graph) has an
+         available Group #2 set G_x (first in array order whose members are all known):
+         C_j = XOR over x of XOR(G_x) = XOR of setXOR(G_x ...)   (the Eq 4 construction)
+    Rounds of [one A sweep, one B sweep] repeat while either resolves something.  Then
+      C  each wanted intermediate x, in the given order: XOR of its first available G_x.
+    A source-free recipe stands for the all-zero symbol.  level(x) = 1 + max level of its
+    sources (known coded symbols: level 0).
+    Returns ([(target kind 'c'|'i', index, sources)], unknown coded set, unresolved wanted)."""
+    sets = parse_check_data(arr)
+    g3 = [m for kind, _, m in sets if kind == 3]
+    g2 = [(x, m) for kind, x, m in sets if kind == 2]
+    unknown = set(int(e) for e in erased)
+    level, steps = {}, []
+
+    def lv(srcs):
+        return 1 + max([level.get(c, 0) for c in srcs] + [0])
+
+    def avail_g2(x):
+        for xx, m in g2:
+            if xx == x and not any(c in unknown for c in m):
+                return m
+        return None
+
+    progress = True
+    while progress and unknown:
+        progress = False
+        for mem in g3:                                                       # A
+            miss = [c for c in mem if c in unknown]
+            if len(miss) == 1:
+                x = miss[0]
+                srcs = [c for c in mem if c != x]
+                level[x] = lv(srcs)
+                steps.append(("c", x, srcs))
+                unknown.discard(x)
+                progress = True
+        for j in sorted(unknown):                                            # B
+            parts = [avail_g2(int(x)) for x in g.lt_row(j)]
+            if all(m is not None for m in parts):
+                srcs = sorted(set_xor(*parts))
+                level[j] = lv(srcs)
+                steps.append(("c", j, srcs))
+                unknown.discard(j)
+                progress = True
+    missing = []
+    for x in want:                                                           # C
+        m = avail_g2(int(x))
+        if m is None:
+            missing.append(int(x))
+        else:
+            steps.append(("i", int(x), list(m)))
+    return steps, unknown, missing
+
+
+def repair(g, arr, erased, coded, want=()):
+    """Execute repair_plan on coded [n, t] (erased rows are ignored): returns (coded copy with
+    the repaired rows, wanted intermediate symbols [len(want), t], unknown coded set)."""
+    steps, unknown, missing = repair_plan(g, arr, erased, want)
+    y = np.array(coded, dtype=np.uint8, copy=True)
+    inter = {}
+    for kind, x, srcs in steps:
+        acc = np.zeros(y.shape[1], dtype=np.uint8)
+        for c in srcs:
+            acc ^= y[c]
+        if kind == "c":
+            y[x] = acc
+        else:
+            inter[x] = acc
+    I = np.zeros((len(want), y.shape[1]), dtype=np.uint8)
+    for r, x in enumerate(want):
+        if int(x) in inter:
+            I[r] = inter[int(x)]
+    return y, I, unknown
