@@ -232,6 +232,93 @@ FSB_API fs_status fs_decode(const fs_decode_plan *plan, uint32_t num_stripes, co
                             uint64_t coded_stride, uint8_t *d_inter, uint64_t inter_stride, void *stream);
 FSB_API void fs_decode_plan_free(fs_decode_plan *plan);  /* NULL-safe */
 
+/* ------------------------------------------------ repair, update, degraded read (NEXT-3)
+ * Check #2 / Check #3 local sets from Algorithm 4, CGA,
+ * run on the host over B = the LT generator (K x n; the paper's k is our K = k+p, reading R19).
+ * A weight-0 column j of CGA's B gives a Group #3 set {C_s : l_{s,j} = 1} (coded symbols whose
+ * XOR is zero); a weight-1 column (symbol x) a Group #2 set: I_x = XOR of its coded symbols.
+ * Optional derived Group #3 sets: FS_CHECKS_M1 = degree-one coded nodes
+ * (G_x setXOR {j}), FS_CHECKS_M2 = check #1 groups (setXOR of the members' G_x, Eq 4).  The sets
+ * are serialised in the <filename>_check.data format: Group #3 as
+ * [0, deg, c_1..c_deg], Group #2 as [1, x, deg, c_1..c_deg], smallest cardinality first
+ * (ties by CGA column, derived sets after, reading R20).  CGA is a heuristic: it
+ * may stop before every column has weight <= 1 (the info reports how far it got).          */
+#define FS_CHECKS_M1 1u
+#define FS_CHECKS_M2 2u
+
+typedef struct fs_checks fs_checks;  /* opaque, immutable after creation */
+
+typedef struct {
+  uint32_t sweeps;           /* passes of CGA's while loop                                      */
+  uint32_t zero_columns;     /* weight-0 columns at exit (the loop's target is n - K)           */
+  uint32_t weight1_columns;  /* weight-1 columns at exit                                        */
+  uint32_t group2;           /* Group #2 sets in the data                                       */
+  uint32_t group3;           /* Group #3 sets in the data (incl. derived)                       */
+  uint32_t derived;          /* derived Group #3 sets (FS_CHECKS_M1 / _M2)                      */
+  uint64_t len;              /* int32 entries of the check data                                 */
+} fs_checks_info;
+
+/* Run CGA on g's LT graph and build the check data.  flags: FS_CHECKS_M1 | FS_CHECKS_M2.
+ * Host only, deterministic.  FS_EINVAL on NULL arguments or unknown flags.                    */
+FSB_API fs_status fs_checks_create(const fs_graph *g, uint32_t flags, fs_checks **out);
+/* Adopt check data produced elsewhere (e.g. by an earlier graph, for an update): validated
+ * against g (flags 0/1, sizes >= 1, coded indices < n, symbols < K); copied.  FS_EINVAL if not. */
+FSB_API fs_status fs_checks_from_data(const fs_graph *g, const int32_t *data, uint64_t len, fs_checks **out);
+/* Host view of the check data (owned by c, valid until fs_checks_free). */
+FSB_API fs_status fs_checks_data(const fs_checks *c, const int32_t **data, uint64_t *len);
+FSB_API fs_status fs_checks_info_get(const fs_checks *c, fs_checks_info *info);
+FSB_API void fs_checks_free(fs_checks *c);  /* NULL-safe */
+
+/* Repair plan (reading R21) for graph g (its LT rows are the base
+ * graph; for an update, g is the extended graph and c the check data of the original code):
+ * unknowns = the erased coded symbols (erased[j] != 0, n bytes, host).  Rounds of
+ *   A: each Group #3 set, in order, with exactly one unknown member repairs it (XOR of the rest);
+ *   B: each unknown coded symbol j, ascending, whose every neighbour x has a Group #2 set with
+ *      all members known: C_j = XOR over x of XOR(G_x)   (the Eq 4 setXOR construction)
+ * repeat while either resolves something; then each of the nwant wanted intermediate symbols
+ * want[] (degraded read) from its first Group #2 set with all members known.
+ * Rows run in levels (1 + max level of the sources); the unresolved remain (decode + encode
+ * rebuilds those).  flags: FS_GRAPH_HOST_ONLY = no device copy.                              */
+typedef struct fs_repair_plan fs_repair_plan;  /* opaque, immutable after creation */
+
+typedef struct {
+  uint32_t erased;           /* erased coded symbols                                            */
+  uint32_t repaired;         /* ... the plan rebuilds                                           */
+  uint32_t unrepaired;       /* ... it cannot (no usable local set)                             */
+  uint32_t want_missing;     /* wanted intermediate symbols without a usable Group #2 set       */
+  uint32_t levels;           /* GPU launches per fs_repair                                      */
+  uint32_t rows;             /* plan rows (repaired + wanted rows)                              */
+  uint64_t xor_sources;      /* total sources over all rows                                     */
+} fs_repair_info;
+
+FSB_API fs_status fs_repair_plan_create(const fs_graph *g, const fs_checks *c, const uint8_t *erased,
+                                        const uint32_t *want, uint32_t nwant, uint32_t flags,
+                                        fs_repair_plan **out);
+FSB_API fs_status fs_repair_plan_info(const fs_repair_plan *plan, fs_repair_info *info);
+/* Host views of the plan rows: level_ptr[levels+1], target[rows] (bit 30 set: coded symbol,
+ * clear: intermediate symbol), src_ptr[rows+1], src[...] (coded indices | bit 30, bit 31 marks a
+ * row's last source).  Owned by the plan.                                                    */
+FSB_API fs_status fs_repair_plan_rows(const fs_repair_plan *plan, const uint32_t **level_ptr,
+                                      uint32_t *levels, const int32_t **target, const int32_t **src_ptr,
+                                      const uint32_t **src);
+/* Run the plan on num_stripes stripes, in place: repaired rows are written into d_coded (row j
+ * at d_coded + s*coded_stride + j*t; erased rows are never read before they are written);
+ * wanted intermediate rows into d_inter (row x at d_inter + s*inter_stride + x*t), which may
+ * be NULL when the plan has none.  Strides multiples of 16, >= n*t and (k+p)*t.  One launch
+ * per level on `stream`.                                                                     */
+FSB_API fs_status fs_repair(const fs_repair_plan *plan, uint32_t num_stripes, uint8_t *d_coded,
+                            uint64_t coded_stride, uint8_t *d_inter, uint64_t inter_stride, void *stream);
+FSB_API void fs_repair_plan_free(fs_repair_plan *plan);  /* NULL-safe */
+
+/* Update: the code extended by extra_files output files.  With s =
+ * max(files, 1), the new graph has n' = n + extra_files * n/s rows and files' = s + extra_files;
+ * file i's rows come from stream seed + i (R17), so rows 0..n-1 are exactly g's and the new
+ * rows n..n'-1 are drawn from fresh streams.  Their symbols are computed with fs_encode (row
+ * range [n, n')) from the data, or, with the data not stored, by fs_repair on the new graph
+ * with the original code's check data and rows n..n'-1 marked erased.  flags as for
+ * fs_graph_create.  FS_EINVAL if extra_files == 0 or n' overflows.                           */
+FSB_API fs_status fs_graph_extend(const fs_graph *g, uint32_t extra_files, uint32_t flags, fs_graph **out);
+
 /* Profiling aid (only meaningful when the process runs with FSB_DEBUG=2): copies out and clears
  * n <= 64 counters of the SMEM kernel: for consumer warp w, [2w] = cycles spent waiting for tiles,
  * [2w+1] = total cycles, each summed over all CTAs since the last call.                    */

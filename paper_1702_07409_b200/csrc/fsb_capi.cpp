@@ -332,6 +332,171 @@ void fs_decode_plan_free(fs_decode_plan *d) {
   delete d;
 }
 
+// ------------------------------------------------------------ repair / update (NEXT-3)
+fs_status fs_checks_create(const fs_graph *h, uint32_t flags, fs_checks **out) {
+  fsb::set_error("");
+  if (!h || !out) { set_error("null argument"); return FS_EINVAL; }
+  *out = nullptr;
+  if (flags & ~(FS_CHECKS_M1 | FS_CHECKS_M2)) { set_error("unknown check flags"); return FS_EINVAL; }
+  fs_checks *c = new (std::nothrow) fs_checks();
+  if (!c) { set_error("out of host memory"); return FS_ENOMEM; }
+  fs_status st;
+  try {
+    st = fsb::build_check_data(h->g, flags, c->cd);
+  } catch (const std::bad_alloc &) {
+    st = FS_ENOMEM;
+    set_error("out of host memory");
+  }
+  if (st != FS_OK) {
+    delete c;
+    return st;
+  }
+  c->n = h->g.prm.n;
+  c->K = h->g.prm.k + h->g.prm.p;
+  *out = c;
+  return FS_OK;
+}
+
+fs_status fs_checks_from_data(const fs_graph *h, const int32_t *data, uint64_t len, fs_checks **out) {
+  fsb::set_error("");
+  if (!h || !out || (len && !data)) { set_error("null argument"); return FS_EINVAL; }
+  *out = nullptr;
+  fs_checks *c = new (std::nothrow) fs_checks();
+  if (!c) { set_error("out of host memory"); return FS_ENOMEM; }
+  fs_status st = fsb::parse_check_data(h->g, data, len, c->cd);
+  if (st != FS_OK) {
+    delete c;
+    return st;
+  }
+  c->n = h->g.prm.n;
+  c->K = h->g.prm.k + h->g.prm.p;
+  *out = c;
+  return FS_OK;
+}
+
+fs_status fs_checks_data(const fs_checks *c, const int32_t **data, uint64_t *len) {
+  if (!c) { set_error("null argument"); return FS_EINVAL; }
+  if (data) *data = c->cd.data.empty() ? nullptr : c->cd.data.data();
+  if (len) *len = c->cd.data.size();
+  return FS_OK;
+}
+
+fs_status fs_checks_info_get(const fs_checks *c, fs_checks_info *info) {
+  if (!c || !info) { set_error("null argument"); return FS_EINVAL; }
+  std::memset(info, 0, sizeof(*info));
+  info->sweeps = c->cd.sweeps;
+  info->zero_columns = c->cd.zero_columns;
+  info->weight1_columns = c->cd.weight1_columns;
+  info->group2 = c->cd.group2;
+  info->group3 = c->cd.group3;
+  info->derived = c->cd.derived;
+  info->len = c->cd.data.size();
+  return FS_OK;
+}
+
+void fs_checks_free(fs_checks *c) { delete c; }
+
+fs_status fs_repair_plan_create(const fs_graph *h, const fs_checks *c, const uint8_t *erased, const uint32_t *want,
+                                uint32_t nwant, uint32_t flags, fs_repair_plan **out) {
+  fsb::set_error("");
+  if (!h || !c || !erased || !out || (nwant && !want)) { set_error("null argument"); return FS_EINVAL; }
+  *out = nullptr;
+  if (c->n > h->g.prm.n || c->K != h->g.prm.k + h->g.prm.p) {
+    set_error("check data does not fit the graph (needs the same K and n_checks <= n)");
+    return FS_EINVAL;
+  }
+  fs_repair_plan *r = new (std::nothrow) fs_repair_plan();
+  if (!r) { set_error("out of host memory"); return FS_ENOMEM; }
+  fs_status st;
+  try {
+    st = fsb::build_repair_plan(h->g, c->cd, erased, want, nwant, r->pl, r->rs);
+  } catch (const std::bad_alloc &) {
+    st = FS_ENOMEM;
+    set_error("out of host memory");
+  }
+  if (st == FS_OK && !(flags & FS_GRAPH_HOST_ONLY)) st = fsb::upload_decode_plan(r->pl);
+  if (st != FS_OK) {
+    fsb::free_decode_plan(r->pl);
+    delete r;
+    return st;
+  }
+  *out = r;
+  return FS_OK;
+}
+
+fs_status fs_repair_plan_info(const fs_repair_plan *r, fs_repair_info *info) {
+  if (!r || !info) { set_error("null argument"); return FS_EINVAL; }
+  std::memset(info, 0, sizeof(*info));
+  info->erased = r->rs.erased;
+  info->repaired = r->rs.repaired;
+  info->unrepaired = r->rs.unrepaired;
+  info->want_missing = r->rs.want_missing;
+  info->levels = r->rs.levels;
+  info->rows = r->rs.rows;
+  info->xor_sources = r->rs.xor_sources;
+  return FS_OK;
+}
+
+fs_status fs_repair_plan_rows(const fs_repair_plan *r, const uint32_t **level_ptr, uint32_t *levels,
+                              const int32_t **target, const int32_t **src_ptr, const uint32_t **src) {
+  if (!r) { set_error("null argument"); return FS_EINVAL; }
+  const fsb::DecodePlan &pl = r->pl;
+  if (level_ptr) *level_ptr = pl.level_ptr.data();
+  if (levels) *levels = static_cast<uint32_t>(pl.level_ptr.size() - 1);
+  if (target) *target = pl.target.empty() ? nullptr : pl.target.data();
+  if (src_ptr) *src_ptr = pl.src_ptr.data();
+  if (src) *src = pl.src.empty() ? nullptr : pl.src.data();
+  return FS_OK;
+}
+
+fs_status fs_repair(const fs_repair_plan *r, uint32_t S, uint8_t *d_coded, uint64_t coded_stride, uint8_t *d_inter,
+                    uint64_t inter_stride, void *stream) {
+  fsb::set_error("");
+  fsb::g_launches = 0;
+  if (!r) { set_error("null plan"); return FS_EINVAL; }
+  const fsb::DecodePlan &pl = r->pl;
+  if (pl.device < 0) { set_error("host-only plan has no device copy"); return FS_EUNSUPPORTED; }
+  if (S == 0 || pl.target.empty()) return FS_OK;
+  if (!d_coded || !aligned16(d_coded) || coded_stride < pl.n * pl.t || coded_stride % 16) {
+    set_error("d_coded must be 16-B aligned with coded_stride >= n*t, a multiple of 16");
+    return FS_EINVAL;
+  }
+  bool wants = false;
+  for (int32_t tg : pl.target) wants = wants || !(static_cast<uint32_t>(tg) & fsb::kSrcCoded);
+  if (wants && (!d_inter || !aligned16(d_inter) || inter_stride < static_cast<uint64_t>(pl.K) * pl.t ||
+                inter_stride % 16)) {
+    set_error("d_inter must be 16-B aligned with inter_stride >= (k+p)*t when the plan reads symbols");
+    return FS_EINVAL;
+  }
+  uint32_t launches = 0;
+  fs_status st = fsb::launch_plan(pl, S, d_coded, coded_stride, d_inter, inter_stride, stream, &launches);
+  if (st == FS_OK) fsb::g_launches = launches;
+  return st;
+}
+
+void fs_repair_plan_free(fs_repair_plan *r) {
+  if (!r) return;
+  fsb::free_decode_plan(r->pl);
+  delete r;
+}
+
+fs_status fs_graph_extend(const fs_graph *h, uint32_t extra_files, uint32_t flags, fs_graph **out) {
+  fsb::set_error("");
+  if (!h || !out) { set_error("null argument"); return FS_EINVAL; }
+  *out = nullptr;
+  if (extra_files == 0) { set_error("extra_files must be >= 1"); return FS_EINVAL; }
+  fs_params prm = h->g.prm;  // fin_* point into h's vectors; fs_graph_create copies them
+  const uint32_t s = std::max<uint32_t>(prm.files, 1);
+  const uint64_t n2 = static_cast<uint64_t>(prm.n) + static_cast<uint64_t>(extra_files) * (prm.n / s);
+  if (n2 >= (1ull << 31) || static_cast<uint64_t>(s) + extra_files >= (1ull << 31)) {
+    set_error("extended n too large");
+    return FS_EINVAL;
+  }
+  prm.n = static_cast<uint32_t>(n2);
+  prm.files = s + extra_files;
+  return fs_graph_create(&prm, flags, out);
+}
+
 uint32_t fs_last_launch_count(void) { return fsb::g_launches; }
 
 void fs_free(fs_graph *h) {

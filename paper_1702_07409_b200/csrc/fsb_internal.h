@@ -153,8 +153,42 @@ fs_status upload_decode_plan(DecodePlan &pl);
 void free_decode_plan(DecodePlan &pl);
 fs_status launch_decode(const DecodePlan &pl, uint32_t S, const uint8_t *coded, uint64_t coded_stride,
                         uint8_t *inter, uint64_t inter_stride, void *stream, uint32_t *launches);
+// any plan (decode or repair): per-level fsb_dpg_level launches; repair targets write coded rows
+fs_status launch_plan(const DecodePlan &pl, uint32_t S, uint8_t *coded, uint64_t coded_stride,
+                      uint8_t *inter, uint64_t inter_stride, void *stream, uint32_t *launches);
 }  // namespace fsb
 
 struct fs_decode_plan {
   fsb::DecodePlan pl;
+};
+
+// ------------------------------------------------------------------ repair (NEXT-3, Alg 4)
+namespace fsb {
+struct CgaResult {
+  std::vector<std::vector<int32_t>> b, l;  // final columns of B and L^{(2,3)}, ascending
+  uint32_t sweeps = 0, zero_columns = 0, weight1_columns = 0;
+  uint64_t updates = 0;
+};
+struct ChecksData {
+  std::vector<int32_t> data;  // the <filename>_check.data integer array
+  uint32_t sweeps = 0, zero_columns = 0, weight1_columns = 0, group2 = 0, group3 = 0, derived = 0;
+};
+struct RepairStats {
+  uint32_t erased = 0, repaired = 0, unrepaired = 0, want_missing = 0, levels = 0, rows = 0;
+  uint64_t xor_sources = 0;
+};
+fs_status run_cga(const Graph &g, CgaResult &r);
+fs_status build_check_data(const Graph &g, uint32_t flags, ChecksData &cd);
+fs_status parse_check_data(const Graph &g, const int32_t *data, uint64_t len, ChecksData &cd);
+fs_status build_repair_plan(const Graph &g, const ChecksData &cd, const uint8_t *erased, const uint32_t *want,
+                            uint32_t nwant, DecodePlan &pl, RepairStats &rs);
+}  // namespace fsb
+
+struct fs_checks {
+  fsb::ChecksData cd;
+  uint32_t n = 0, K = 0;
+};
+struct fs_repair_plan {
+  fsb::DecodePlan pl;
+  fsb::RepairStats rs;
 };

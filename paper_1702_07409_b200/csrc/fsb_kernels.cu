@@ -471,7 +471,7 @@ template <uint32_t kBatch, int kMinBlocks>
 __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
     fsb_dpg_level(uint32_t S, uint32_t t, uint32_t nbands, uint32_t row0, uint32_t nrows, uint32_t band_rows,
                   const int32_t *__restrict__ target, const int32_t *__restrict__ src_ptr,
-                  const uint32_t *__restrict__ src, const uint8_t *__restrict__ coded, uint64_t coded_stride,
+                  const uint32_t *__restrict__ src, uint8_t *coded, uint64_t coded_stride,
                   uint8_t *inter, uint64_t inter_stride) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nchunks = (nrows + band_rows - 1) / band_rows;
@@ -486,7 +486,8 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   const uint32_t byte = active ? byte_raw : 0;
   const uint8_t *ibase = inter + s * inter_stride + byte;  // read: rows of earlier levels
   const uint8_t *cbase = coded + s * coded_stride + byte;
-  uint8_t *obase = inter + s * inter_stride + byte_raw;
+  uint8_t *obase = inter + s * inter_stride + byte_raw;  // target m: intermediate row m
+  uint8_t *cobase = coded + s * coded_stride + byte_raw; // target m | kSrcCoded: coded row m (repair)
   const uint32_t r0 = row0 + chunk * band_rows;
   const uint32_t rows = min(band_rows, row0 + nrows - r0);
   const int32_t tg = lane < rows ? __ldg(&target[r0 + lane]) : 0;
@@ -514,7 +515,8 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
         xor_into(acc, v[u]);
         if (fl[u] & kSrcLast) {  // warp-uniform: row complete
           const uint32_t f = static_cast<uint32_t>(__shfl_sync(0xffffffffu, tg, cur));
-          if (active) *reinterpret_cast<uint4 *>(obase + static_cast<uint64_t>(f) * t) = acc;
+          uint8_t *ob = (f & kSrcCoded) ? cobase : obase;
+          if (active) *reinterpret_cast<uint4 *>(ob + static_cast<uint64_t>(f & (kSrcCoded - 1)) * t) = acc;
           acc = make_uint4(0, 0, 0, 0);
           ++cur;
         }
@@ -768,6 +770,12 @@ void free_decode_plan(DecodePlan &pl) {
 
 fs_status launch_decode(const DecodePlan &pl, uint32_t S, const uint8_t *coded, uint64_t coded_stride,
                         uint8_t *inter, uint64_t inter_stride, void *stream_ptr, uint32_t *launches) {
+  // decode plans never target coded rows, so the coded buffer is only read
+  return launch_plan(pl, S, const_cast<uint8_t *>(coded), coded_stride, inter, inter_stride, stream_ptr, launches);
+}
+
+fs_status launch_plan(const DecodePlan &pl, uint32_t S, uint8_t *coded, uint64_t coded_stride,
+                      uint8_t *inter, uint64_t inter_stride, void *stream_ptr, uint32_t *launches) {
   *launches = 0;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   const uint32_t nbands = static_cast<uint32_t>((pl.t + kBandBytes - 1) / kBandBytes);

@@ -23,7 +23,10 @@ EXPORTS = ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get
            "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_last_launch_count",
            "fs_free", "fs_last_error", "fs_version", "fs_graph_schedule", "fs_debug_counters",
            "fs_decode_plan_create", "fs_decode_plan_info", "fs_decode_plan_state", "fs_decode",
-           "fs_decode_plan_free", "fs_encode_range")
+           "fs_decode_plan_free", "fs_encode_range", "fs_checks_create", "fs_checks_from_data",
+           "fs_checks_data", "fs_checks_info_get", "fs_checks_free", "fs_repair_plan_create",
+           "fs_repair_plan_info", "fs_repair_plan_rows", "fs_repair", "fs_repair_plan_free",
+           "fs_graph_extend")
 
 
 class FsError(RuntimeError):
@@ -49,6 +52,18 @@ class fs_graph_info(ctypes.Structure):
                 ("smem_bytes", ctypes.c_uint32), ("sched_bytes", ctypes.c_uint32),
                 ("sched_steps_max", ctypes.c_uint32), ("sched_steps_avg", ctypes.c_uint32),
                 ("device", ctypes.c_int32)]
+
+
+class fs_checks_info(ctypes.Structure):
+    _fields_ = [("sweeps", ctypes.c_uint32), ("zero_columns", ctypes.c_uint32),
+                ("weight1_columns", ctypes.c_uint32), ("group2", ctypes.c_uint32),
+                ("group3", ctypes.c_uint32), ("derived", ctypes.c_uint32), ("len", ctypes.c_uint64)]
+
+
+class fs_repair_info(ctypes.Structure):
+    _fields_ = [("erased", ctypes.c_uint32), ("repaired", ctypes.c_uint32), ("unrepaired", ctypes.c_uint32),
+                ("want_missing", ctypes.c_uint32), ("levels", ctypes.c_uint32), ("rows", ctypes.c_uint32),
+                ("xor_sources", ctypes.c_uint64)]
 
 
 class fs_decode_info(ctypes.Structure):
@@ -92,6 +107,22 @@ def lib():
             getattr(L, f).restype = ctypes.c_int
         L.fs_decode_plan_free.argtypes = [P]
         L.fs_decode_plan_free.restype = None
+        L.fs_checks_create.argtypes = [P, u32, PP]
+        L.fs_checks_from_data.argtypes = [P, P, u64, PP]
+        L.fs_checks_data.argtypes = [P, PP, ctypes.POINTER(u64)]
+        L.fs_checks_info_get.argtypes = [P, ctypes.POINTER(fs_checks_info)]
+        L.fs_repair_plan_create.argtypes = [P, P, P, P, u32, u32, PP]
+        L.fs_repair_plan_info.argtypes = [P, ctypes.POINTER(fs_repair_info)]
+        L.fs_repair_plan_rows.argtypes = [P, PP, ctypes.POINTER(u32), PP, PP, PP]
+        L.fs_repair.argtypes = [P, u32, P, u64, P, u64, P]
+        L.fs_graph_extend.argtypes = [P, u32, u32, PP]
+        for f in ("fs_checks_create", "fs_checks_from_data", "fs_checks_data", "fs_checks_info_get",
+                  "fs_repair_plan_create", "fs_repair_plan_info", "fs_repair_plan_rows", "fs_repair",
+                  "fs_graph_extend"):
+            getattr(L, f).restype = ctypes.c_int
+        for f in ("fs_checks_free", "fs_repair_plan_free"):
+            getattr(L, f).argtypes = [P]
+            getattr(L, f).restype = None
         L.fs_debug_counters.argtypes = [P, u32]
         L.fs_debug_counters.restype = ctypes.c_int
         L.fs_last_launch_count.restype = u32
@@ -217,6 +248,15 @@ class Graph:
                                      (3 * nwarps.value,)).copy()
         return words, cb.value, info.reshape(-1, 3), kpad.value, z0.value
 
+    def extend(self, extra_files, host_only=False):
+        """fs_graph_extend (update): the graph with extra_files more output files."""
+        s = max(int(self.cfg.get("files", 1)), 1)
+        cfg = dict(self.cfg, n=self.n + extra_files * (self.n // s), files=s + extra_files)
+        h = ctypes.c_void_p()
+        _check(lib().fs_graph_extend(self._h, extra_files, FS_GRAPH_HOST_ONLY if host_only else 0,
+                                     ctypes.byref(h)))
+        return Graph(h, cfg)
+
     def set_variant(self, variant):
         _check(lib().fs_graph_set_variant(self._h, variant))
 
@@ -296,6 +336,113 @@ class DecodePlan:
     def free(self):
         if self._h:
             lib().fs_decode_plan_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+CHECKS_M1, CHECKS_M2 = 1, 2
+
+
+class Checks:
+    """Owner of an fs_checks: CGA (Alg 4) local sets in the <filename>_check.data format."""
+
+    def __init__(self, handle, graph):
+        self._h = handle
+        self.graph = graph
+
+    @classmethod
+    def create(cls, graph, flags=0):
+        h = ctypes.c_void_p()
+        _check(lib().fs_checks_create(graph._h, flags, ctypes.byref(h)))
+        return cls(h, graph)
+
+    @classmethod
+    def from_data(cls, graph, data):
+        a = np.ascontiguousarray(data, dtype=np.int32)
+        h = ctypes.c_void_p()
+        _check(lib().fs_checks_from_data(graph._h, a.ctypes.data_as(ctypes.c_void_p) if a.size else None,
+                                         a.size, ctypes.byref(h)))
+        return cls(h, graph)
+
+    def data(self):
+        p, n = ctypes.c_void_p(), ctypes.c_uint64()
+        _check(lib().fs_checks_data(self._h, ctypes.byref(p), ctypes.byref(n)))
+        if not n.value:
+            return np.zeros(0, np.int32)
+        return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_int32)), (n.value,)).copy()
+
+    def info(self):
+        inf = fs_checks_info()
+        _check(lib().fs_checks_info_get(self._h, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in fs_checks_info._fields_}
+
+    def free(self):
+        if self._h:
+            lib().fs_checks_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class RepairPlan:
+    """Owner of an fs_repair_plan (repair / update / degraded read, NEXT-3)."""
+
+    def __init__(self, graph, checks, erased, want=(), host_only=False):
+        er = np.ascontiguousarray(np.asarray(erased, dtype=bool).astype(np.uint8))
+        if er.shape != (graph.n,):
+            raise ValueError("erased must have n entries")
+        w = np.ascontiguousarray(want, dtype=np.uint32)
+        self.graph = graph
+        self._h = None
+        h = ctypes.c_void_p()
+        _check(lib().fs_repair_plan_create(graph._h, checks._h, er.ctypes.data_as(ctypes.c_void_p),
+                                           w.ctypes.data_as(ctypes.c_void_p) if w.size else None, w.size,
+                                           FS_GRAPH_HOST_ONLY if host_only else 0, ctypes.byref(h)))
+        self._h = h
+
+    def info(self):
+        inf = fs_repair_info()
+        _check(lib().fs_repair_plan_info(self._h, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in fs_repair_info._fields_}
+
+    def rows(self):
+        """(level_ptr, target, src_ptr, src) copies; see include/fsb.h for the flags."""
+        lp, tg, sp, sr = (ctypes.c_void_p() for _ in range(4))
+        nl = ctypes.c_uint32()
+        _check(lib().fs_repair_plan_rows(self._h, ctypes.byref(lp), ctypes.byref(nl), ctypes.byref(tg),
+                                         ctypes.byref(sp), ctypes.byref(sr)))
+
+        def arr(p, n, ct):
+            if n == 0 or not p.value:
+                return np.zeros(0, dtype=np.dtype(ct))
+            return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ct)), (n,)).copy()
+
+        level_ptr = arr(lp, nl.value + 1, ctypes.c_uint32)
+        rows = int(level_ptr[-1]) if len(level_ptr) else 0
+        target = arr(tg, rows, ctypes.c_int32)
+        src_ptr = arr(sp, rows + 1, ctypes.c_int32)
+        src = arr(sr, int(src_ptr[-1]) if rows else 0, ctypes.c_uint32)
+        return level_ptr, target, src_ptr, src
+
+    def repair(self, coded, inter=None, stream=None):
+        """fs_repair in place over contiguous [S,n,t] coded (and [S,K,t] inter) CUDA tensors."""
+        S = coded.shape[0]
+        t = self.graph.t
+        _check(lib().fs_repair(self._h, S, _ptr(coded), self.graph.n * t, _ptr(inter), self.graph.K * t,
+                               _stream(stream)))
+
+    def free(self):
+        if self._h:
+            lib().fs_repair_plan_free(self._h)
             self._h = None
 
     def __del__(self):
