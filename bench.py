@@ -202,20 +202,32 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--op", default="encode", choices=["encode", "decode"],
-                    help="decode: time fs_decode (Alg 5 DPG plan) instead of the encode (NEXT-1)")
+    ap.add_argument("--op", default="encode", choices=["encode", "decode", "repair", "update"],
+                    help="decode: time fs_decode (Alg 5 DPG plan, NEXT-1); repair: fs_repair of "
+                         "--erase-frac erased coded symbols; update: fs_repair of one extra output "
+                         "file from the original check data (NEXT-3)")
+    ap.add_argument("--erase-frac", type=float, default=0.01,
+                    help="repair: fraction of coded symbols erased (seeded random subset)")
     ap.add_argument("--recv-frac", type=float, default=0.95,
                     help="decode: fraction of coded symbols received (seeded random subset)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.op == "decode" and "--config" not in sys.argv:
         args.config = 5
+    if args.op in ("repair", "update") and "--config" not in sys.argv:
+        args.config = 7
     cfg = configs.get(args.config)
     if args.op == "decode":
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "decode reference arm not implemented"}))
             return
         run_decode(args, cfg)
+        return
+    if args.op in ("repair", "update"):
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "repair reference arm not implemented"}))
+            return
+        run_repair(args, cfg)
         return
 
     if args.impl == "reference":
@@ -403,6 +415,87 @@ def run_decode(args, cfg):
            "roofline": {"bound": "hbm", "achieved": round(b_hbm / (ms * 1e-3) / 1e9, 1), "peak": peak,
                         "unit": "GB/s", "frac": round(b_hbm / (ms * 1e-3) / 1e9 / peak, 4),
                         "algorithmic_bytes_per_step": b_hbm, "peak_source": peak_src,
+                        "kernel": "fsb_dpg_level x %d launches" % launches},
+           "gpu_launches": launches * args.steps, "checked": ok, "clocks": clk}
+    print(json.dumps(out))
+
+
+def run_repair(args, cfg):
+    """NEXT-3 on one GPU.  repair: a seeded random --erase-frac of the coded symbols is erased and
+    rebuilt from the local sets (CGA check data); update: the code is extended by one
+    output file whose symbols are computed from the ORIGINAL code's check data
+    (the data is not read).  One step = one fs_repair call (one launch per level) over every
+    stripe.  Metric: rebuilt coded bytes per second."""
+    import numpy as np
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    g0 = fsb.Graph.create(cfg)
+    t_cga = time.perf_counter()
+    checks0 = fsb.Checks.create(g0, fsb.CHECKS_M1 | fsb.CHECKS_M2)
+    t_cga = time.perf_counter() - t_cga
+    if args.op == "update":
+        g = g0.extend(1)
+        checks = fsb.Checks.from_data(g, checks0.data())
+        erased = np.zeros(g.n, bool)
+        erased[g0.n:] = True
+    else:
+        g, checks = g0, checks0
+        rng = np.random.default_rng(cfg["seed"] + 1)
+        erased = np.zeros(g.n, bool)
+        erased[rng.choice(g.n, max(1, int(round(args.erase_frac * g.n))), replace=False)] = True
+    k, p, n, t, S = g.k, g.p, g.n, g.t, cfg["stripes"]
+    t_plan = time.perf_counter()
+    plan = fsb.RepairPlan(g, checks, erased)
+    t_plan = time.perf_counter() - t_plan
+    inf = plan.info()
+    data = inputs.stripe_data(cfg, device=dev)
+    chk = torch.empty((S, p, t), dtype=torch.uint8, device=dev) if p else None
+    ref = torch.empty((S, n, t), dtype=torch.uint8, device=dev)
+    g.encode_stripes(data, chk, ref)                              # expected symbols (untimed)
+    del data, chk
+    er_t = torch.from_numpy(erased).to(dev)
+    cod = ref.clone()
+    cod[:, er_t] = 0
+    stream = torch.cuda.Stream(device=dev)
+    for _ in range(args.warmup):
+        plan.repair(cod, stream=stream)
+    launches = fsb.last_launch_count()
+    stream.synchronize()
+    level_ptr, target, src_ptr, src = plan.rows()
+    rebuilt = [int(x) & 0x3FFFFFFF for x in target]
+    ok = bool(torch.equal(cod[:, rebuilt], ref[:, rebuilt])) if rebuilt else True
+    del ref
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    with torch.cuda.stream(stream):
+        evs[0].record(stream)
+        for i in range(args.steps):
+            plan.repair(cod, stream=stream)
+            evs[i + 1].record(stream)
+    stream.synchronize()
+    clk = clocks.stop()
+    ms = evs[0].elapsed_time(evs[-1]) / args.steps
+    rows = len(rebuilt)
+    distinct_src = len(set(int(v) & 0x3FFFFFFF for v in src))
+    value = S * rows * t / (ms * 1e-3) / 1e9
+    b_hbm = S * (distinct_src + rows) * t               # each source row read once + each rebuilt row written
+    b_gather = S * int(inf["xor_sources"]) * t
+    peak, peak_src = _peaks()
+    out = {"op": args.op, "metric": "%s throughput, rebuilt coded GB/s (CGA local sets)" % args.op,
+           "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(ms, 5), "higher_is_better": True, "dtype": "u8", "data": DATA,
+           "config": {"workload": cfg["name"], "k": k, "p": p, "n": n, "t": t, "stripes": S,
+                      "files": g.cfg.get("files", 1), "erased": inf["erased"], "rebuilt": inf["repaired"],
+                      "unrepaired": inf["unrepaired"], "levels": inf["levels"], "xor_sources": inf["xor_sources"],
+                      "distinct_sources": distinct_src, "cga_s": round(t_cga, 3), "plan_s": round(t_plan, 4),
+                      "checks": checks0.info()},
+           "roofline": {"bound": "hbm", "achieved": round(b_hbm / (ms * 1e-3) / 1e9, 1), "peak": peak,
+                        "unit": "GB/s", "frac": round(b_hbm / (ms * 1e-3) / 1e9 / peak, 4),
+                        "algorithmic_bytes_per_step": b_hbm, "peak_source": peak_src,
+                        "gather_bytes_per_step": b_gather,
+                        "gather_GBps": round(b_gather / (ms * 1e-3) / 1e9, 1),
                         "kernel": "fsb_dpg_level x %d launches" % launches},
            "gpu_launches": launches * args.steps, "checked": ok, "clocks": clk}
     print(json.dumps(out))

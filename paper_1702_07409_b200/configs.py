@@ -32,6 +32,10 @@ CONFIGS = {
     # (b, k) = (962, 1036): P=37, k'=28, j'=2, 74 checks of 26 members in 2 levels.
     6: dict(name="c6_array_precode", k=962, p=74, d_p=26, n=1280, t=4096, dist=RSD,
             rsd_c=0.1, rsd_delta=0.05, seed=6, stripes=256, precode="array"),
+    # Not a BASELINE config: the NEXT-3 measurement workload -- config 2's code (CGA converges on
+    # it) written as s = 10 output files (per-file streams, R17), 256 stripes of 4 KiB symbols.
+    7: dict(name="c7_repair", k=1000, p=20, d_p=3, n=1300, t=4096, dist=RSD,
+            rsd_c=0.05, rsd_delta=0.01, seed=2, stripes=256, files=10),
 }
 
 

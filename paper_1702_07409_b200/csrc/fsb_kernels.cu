@@ -496,7 +496,8 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   uint32_t cur = 0;
   uint4 acc = make_uint4(0, 0, 0, 0);
   for (int32_t e0 = base; e0 < end; e0 += 32) {
-    const uint32_t cv = e0 + static_cast<int32_t>(lane) < end ? __ldg(&src[e0 + lane]) : 0u;
+    // past-the-end lanes name coded row 0 (always a valid address; d_inter may be NULL in repair)
+    const uint32_t cv = e0 + static_cast<int32_t>(lane) < end ? __ldg(&src[e0 + lane]) : kSrcCoded;
     const int32_t nb = min(32, end - e0);
     for (int32_t kk = 0; kk < nb; kk += kBatch) {
       uint4 v[kBatch];
