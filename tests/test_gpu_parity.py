@@ -343,3 +343,66 @@ def test_array_precode_parity(S):
         _, c, y = _run(cfg, v, data=torch.from_numpy(D).cuda())
         _assert_equal(c, C, "array checks v%d" % v)
         _assert_equal(y, Y, "array coded v%d" % v)
+
+
+def _check_supports(pre_rp, pre_c, k, p):
+    """Data support of each check over GF(2): members < k, or (array precode, Alg 2) an earlier
+    check whose support is XORed in."""
+    sup = []
+    for i in range(p):
+        acc = set()
+        for m in pre_c[pre_rp[i]:pre_rp[i + 1]]:
+            m = int(m)
+            acc ^= {m} if m < k else sup[m - k]
+        sup.append(acc)
+    return sup
+
+
+def _effective_support(csup, lt_rp, lt_c, k, j):
+    """Data symbols of G_eff row j = G_LT . [I_k ; G_pre] over GF(2)."""
+    odd = set()
+    for m in lt_c[lt_rp[j]:lt_rp[j + 1]]:
+        m = int(m)
+        odd ^= {m} if m < k else csup[m - k]
+    return odd
+
+
+@pytest.mark.parametrize("cid", [2, 4, 5, 6])
+def test_bit_probe_full_scale(cid):
+    """P6 at full size, oracle-free: data symbol i = one-hot bit i (k <= 8t), so bit i of Y_j must
+    be G_eff[j][i] -- computed from the CSR alone -- on sampled rows (all rows for c2/c4/c6, 3000
+    rows incl. the highest-degree ones for c5), in the launch configuration bench.py times."""
+    _need_gpu()
+    cfg = dict(configs.get(cid), stripes=1)
+    g = fsb.Graph.create(cfg)
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    assert k <= 8 * t
+    idx = torch.arange(k, device="cuda")
+    d = torch.zeros((1, k, t), dtype=torch.uint8, device="cuda")
+    d[0, idx, idx // 8] = (1 << (idx % 8)).to(torch.uint8)
+    chk = torch.empty((1, p, t), dtype=torch.uint8, device="cuda") if p else None
+    cod = torch.empty((1, n, t), dtype=torch.uint8, device="cuda")
+    g.encode_stripes(d, chk, cod)
+    torch.cuda.synchronize()
+    pre_rp, pre_c, lt_rp, lt_c = g.csr()
+    csup = _check_supports(pre_rp, pre_c, k, p)
+    if n <= 2000:
+        rows = np.arange(n)
+    else:
+        deg = np.diff(lt_rp)
+        rows = np.unique(np.concatenate([np.argsort(-deg)[:200],
+                                         np.random.default_rng(cid).choice(n, 2800, replace=False)]))
+    got = np.unpackbits(cod[0, torch.from_numpy(rows).cuda()].cpu().numpy(), axis=1, bitorder="little")
+    for r, j in enumerate(rows):
+        want = np.zeros(8 * t, np.uint8)
+        sup = _effective_support(csup, lt_rp, lt_c, k, int(j))
+        if sup:
+            want[list(sup)] = 1
+        assert np.array_equal(got[r], want), "row %d" % j
+    if p:
+        cb = np.unpackbits(chk[0].cpu().numpy(), axis=1, bitorder="little")
+        for i in range(p):
+            want = np.zeros(8 * t, np.uint8)
+            if csup[i]:
+                want[list(csup[i])] = 1
+            assert np.array_equal(cb[i], want), "check %d" % i

@@ -62,6 +62,16 @@ __global__ void __launch_bounds__(512, 1) mix(uint4* out, int rows, int iters) {
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
+    if (V == 9 || V == 10 || V == 11) {  // as 6 with explicit cache operators
+      const uint32_t row = (hw + (threadIdx.x >> 2) * 7919u) & 2047u;
+      uint4* dst = out + ((row * 256 + blockIdx.x * 4 + lane4) & (1024 * 512 - 1));
+      if (V == 9)
+        asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(acc.x), "r"(acc.y), "r"(acc.z), "r"(acc.w) : "memory");
+      if (V == 10)
+        asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(acc.x), "r"(acc.y), "r"(acc.z), "r"(acc.w) : "memory");
+      if (V == 11)
+        asm volatile("st.global.wt.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(acc.x), "r"(acc.y), "r"(acc.z), "r"(acc.w) : "memory");
+    }
     if (V == 7) {
       const uint32_t row = (hw + (threadIdx.x >> 3) * 7919u) & 2047u;
       out[(row * 256 + blockIdx.x * 8 + (lane & 7)) & (1024 * 512 - 1)] = acc;
@@ -94,6 +104,6 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   uint4* out; cudaMalloc(&out, 1024 * 512 * 16);
   run<0>(out, sms); run<1>(out, sms); run<2>(out, sms); run<3>(out, sms); run<5>(out, sms);
-  run<6>(out, sms); run<7>(out, sms); run<8>(out, sms);
+  run<6>(out, sms); run<7>(out, sms); run<8>(out, sms); run<9>(out, sms); run<10>(out, sms); run<11>(out, sms);
   return 0;
 }
