@@ -15,7 +15,7 @@ namespace fsb {
 constexpr int kSliceBytes = 64;
 constexpr int kUnitRows = 64;
 constexpr int kUnitBytes = kUnitRows * kSliceBytes;     // 4 KiB
-constexpr int kConsumerWarps = 20;
+constexpr int kConsumerWarps = 24;
 constexpr int kHalvesPerWarp = 8;                        // half-groups: 4 lanes x 16 B = 64 B
 constexpr int kPrecodeWarps = 3;                         // precode (a3) warps per CTA
 constexpr int kThreads = (kConsumerWarps + 1 + kPrecodeWarps) * 32;  // + 1 TMA warp

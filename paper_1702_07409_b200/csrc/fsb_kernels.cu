@@ -102,6 +102,23 @@ __device__ __forceinline__ void xor_into(uint4 &a, const uint4 &b) {
 __device__ __forceinline__ void st_stream(uint8_t *p, const uint4 &v) {
   __stcs(reinterpret_cast<uint4 *>(p), v);
 }
+// Tensor memory (TMEM): 16 B per lane at 4 consecutive 32-bit columns of this warp's lane quarter.
+// tcgen05.ld/st do not use the L1TEX/LSU pipe the gathers saturate (tools/microbench/mb8.cu).
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint4 &v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 tmem_ld16(uint32_t taddr) {
+  uint4 v;
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "r"(taddr)
+      : "memory");
+  return v;
+}
 
 // ============================================================================ SMEM kernel
 // Profiling experiments only (FSB_DEBUG=2): per consumer warp, cycles spent waiting for a tile
@@ -121,6 +138,8 @@ struct SmemArgs {
   uint32_t nslices, ntiles, p, d_p, kpad, zero_even, data_units, tile_units;
   uint32_t slice0;             // first 64-B slice of the column range
   uint32_t sched_chunks, cont_base;
+  uint32_t paired;             // 1: tiles come in adjacent-slice pairs, full 128-B line stores
+  uint32_t tmem_cols;          // TMEM columns allocated per CTA in paired mode (power of 2)
   uint32_t debug;              // FSB_DEBUG bits (profiling experiments only; 0 in production)
   uint32_t wait_ns;            // consumer sleep between probes of a tile's `ready` barrier
 };
@@ -178,9 +197,16 @@ __device__ __forceinline__ void gather_xor_n(uint4 &acc, const uint4 &c, uint32_
 }
 
 // One item (fsb_internal.h): head chunk h, continuation chunks at *cp (shared address, advanced),
-// XOR in registers, one 64-B store per half-group (split items: combined over the 8 halves).
+// XOR in registers, then the row results leave according to kMode:
+// (kMode is warp-uniform and a runtime value: one inlined copy serves all three modes)
+//   0 (unpaired): one 64-B store per half-group (split items: combined over the halves);
+//   1 (paired, the pair's first tile): nothing leaves; each lane parks its 16 B in TMEM block `tcol`;
+//   2 (paired, second tile = the other 64-B half of the same 128-B lines, read with the partner
+//     half-group's schedule, so half-group h holds row R_{h^1}): each row leaves as one full 128-B
+//     line -- the first tile's half from TMEM (the lane's own row) next to the partner's second
+//     half -- two stores per item.
 __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t sbase, uint8_t *out, uint64_t t,
-                                        uint32_t half_id) {
+                                        uint32_t half_id, uint32_t tcol, int kMode, uint32_t first) {
   const uint32_t row = h.x & 0xFFFFu;
   const uint32_t ctrl = h.x >> 16;
   const uint32_t L = ctrl & kMaxItemLen;
@@ -198,7 +224,8 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
     }
     gather_xor_n<0>(acc, c, rem, sbase);
   }
-  if (ctrl & kSplitBit) {  // warp-split row: combine the eight half-groups' partial XORs
+  const bool wsplit = ctrl & kSplitBit;
+  if (wsplit) {  // warp-split row: combine the eight half-groups' partial XORs (all lanes get it)
 #pragma unroll
     for (int o = 4; o <= 16; o <<= 1) {
       acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -206,10 +233,7 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
       acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, o);
       acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, o);
     }
-    if (half_id == 0) st_stream(out + static_cast<uint64_t>(row) * t, acc);
-    return;
-  }
-  if (ctrl & kPairSplitBit) {  // pair-split groups: half 0 takes its partner half's part
+  } else if (ctrl & kPairSplitBit) {  // pair-split groups: both halves take the partner's part
     uint4 o;
     o.x = __shfl_xor_sync(0xffffffffu, acc.x, 4);
     o.y = __shfl_xor_sync(0xffffffffu, acc.y, 4);
@@ -217,7 +241,48 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
     o.w = __shfl_xor_sync(0xffffffffu, acc.w, 4);
     if (h.y & kPairFlag) xor_into(acc, o);
   }
-  if (row != kNoRow) st_stream(out + static_cast<uint64_t>(row) * t, acc);
+  if (kMode == 0) {
+    if (wsplit) {
+      if (half_id == 0) st_stream(out + static_cast<uint64_t>(row) * t, acc);
+    } else if (row != kNoRow) {
+      st_stream(out + static_cast<uint64_t>(row) * t, acc);
+    }
+  } else if (kMode == 1) {
+    tmem_st16(tcol, acc);
+  } else {
+    const uint4 prev = tmem_ld16(tcol);                                   // own row, slice s
+    const uint32_t own = __shfl_xor_sync(0xffffffffu, row, 4);            // R_h (row = R_{h^1})
+    const bool hi = half_id & 1;
+    const uint32_t ra = hi ? row : own, rb = hi ? own : row;              // R_{2q}, R_{2q+1}
+    // `first` = byte offset in the line of the pair's first tile (0: slice s first, 64: s+1 first)
+    const uint32_t second = kSliceBytes - first;
+    // line of R_{2q}: even half-group its first-tile half (TMEM), odd half-group the second (computed)
+    if (ra != kNoRow && (!wsplit || half_id < 2))
+      st_stream(out + static_cast<uint64_t>(ra) * t + (hi ? second : first), hi ? acc : prev);
+    // line of R_{2q+1}: even half-group the second-tile half (computed), odd half-group its first (TMEM)
+    if (rb != kNoRow && !wsplit)
+      st_stream(out + static_cast<uint64_t>(rb) * t + (hi ? first : second), hi ? prev : acc);
+  }
+}
+
+// Tile i of this CTA: (stripe, slice).  Unpaired: tile blockIdx.x + i*gridDim.x of S x nslices.
+// Paired: pair blockIdx.x + (i/2)*gridDim.x of S x nslices/2, slice 2*(pair % (nslices/2)) plus
+// (i&1), flipped on odd CTAs: half the SMs write their lines while the other half park, so the
+// HBM write stream stays even instead of pulsing with the tile pairs.
+__device__ __forceinline__ bool tile_of(const SmemArgs &a, uint32_t i, uint32_t &stripe, uint32_t &slice) {
+  if (a.paired) {
+    const uint32_t pair = blockIdx.x + (i >> 1) * gridDim.x;
+    const uint32_t nsp = a.nslices >> 1;
+    if (pair >= (a.ntiles >> 1)) return false;
+    stripe = pair / nsp;
+    slice = a.slice0 + 2 * (pair % nsp) + ((i ^ blockIdx.x) & 1);
+    return true;
+  }
+  const uint32_t tile = blockIdx.x + i * gridDim.x;
+  if (tile >= a.ntiles) return false;
+  stripe = tile / a.nslices;
+  slice = a.slice0 + tile % a.nslices;
+  return true;
 }
 
 // Persistent encode kernel, one CTA per SM.  Shared memory: two tile buffers (tile_units x 4 KiB
@@ -239,8 +304,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t pre_n = a.p * a.d_p;
   uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(pre_s) + ((pre_n * 2 + 15) & ~15u));
   uint64_t *full = bars, *ready = bars + 2, *empty = bars + 4;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 6);  // TMEM base address (paired mode)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t smem_base = smem_u32(smem);
+  if (a.paired && warp == 0) {  // one warp allocates the CTA's TMEM columns (one CTA per SM)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(a.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
@@ -258,16 +330,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t b = threadIdx.x >> 3, r = (threadIdx.x >> 2) & 1, l4 = threadIdx.x & 3;
     sts128(smem_base + b * buf_bytes + (a.zero_even + r) * kSliceBytes + l4 * 16, make_uint4(0, 0, 0, 0));
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   if (warp == kConsumerWarps) {
     // ---------------------------------------------------------------- TMA warp (one lane)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-      uint32_t i = 0;
-      for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
+      uint32_t stripe, slice;
+      for (uint32_t i = 0; tile_of(a, i, stripe, slice); ++i) {
         const uint32_t b = i & 1, ph = (i >> 1) & 1;
-        const uint32_t stripe = tile / a.nslices, slice = a.slice0 + tile % a.nslices;
         const uint32_t buf = smem_base + b * buf_bytes;
         mbar_wait(smem_u32(&empty[b]), ph ^ 1);  // consumers released tile i-2
         if (a.debug & 1) {  // experiment: no TMA (consumers gather stale rows)
@@ -289,10 +362,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // `ready`.  Separate from the TMA warp so the next tile's loads never wait for this work.
     const uint32_t pw = warp - kConsumerWarps - 1;                  // precode warp 0..kPrecodeWarps-1
     const uint32_t half_id = pw * kHalvesPerWarp + (lane >> 2), lane4 = lane & 3;
-    uint32_t i = 0;
-    for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
+    uint32_t stripe, slice;
+    for (uint32_t i = 0; tile_of(a, i, stripe, slice); ++i) {
       const uint32_t b = i & 1, ph = (i >> 1) & 1;
-      const uint32_t stripe = tile / a.nslices, slice = a.slice0 + tile % a.nslices;
       const uint32_t buf = smem_base + b * buf_bytes;
       mbar_wait(smem_u32(&full[b]), ph);
       // precode, level by level (a check may read checks of earlier levels, Alg 2): check c of
@@ -330,36 +402,57 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ------------------------------------------------------------------- consumer warps
   const uint32_t half_id = lane >> 2, lane4 = lane & 3;
   const uint32_t nitems = __ldg(&a.warp_info[warp * 3 + 0]);
-  const uint32_t head0 = smem_u32(sched_s) + __ldg(&a.warp_info[warp * 3 + 1]) * kChunkBytes + half_id * 16;
-  const uint32_t cont0 =
-      smem_u32(sched_s) + (a.cont_base + __ldg(&a.warp_info[warp * 3 + 2])) * kChunkBytes + half_id * 16;
-  uint32_t i = 0;
+  const uint32_t head_b = smem_u32(sched_s) + __ldg(&a.warp_info[warp * 3 + 1]) * kChunkBytes;
+  const uint32_t cont_b = smem_u32(sched_s) + (a.cont_base + __ldg(&a.warp_info[warp * 3 + 2])) * kChunkBytes;
+  // TMEM: this warp's lane quarter (warp % 4) and its column block after the earlier warps of the
+  // same quarter (4 columns = 16 B per lane per item)
+  uint32_t tcol0 = 0;
+  if (a.paired) {
+    uint32_t col = 0;
+    for (int w = warp & 3; w < warp; w += 4) col += 4 * __ldg(&a.warp_info[w * 3 + 0]);
+    tcol0 = *tmem_slot + ((32u * (warp & 3)) << 16) + col;
+  }
   const long long t_start = (a.debug & 2) ? clock64() : 0;
-  for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++i) {
+  uint32_t stripe, slice;
+  for (uint32_t i = 0; tile_of(a, i, stripe, slice); ++i) {
     const uint32_t b = i & 1, ph = (i >> 1) & 1;
-    const uint32_t stripe = tile / a.nslices, slice = a.slice0 + tile % a.nslices;
+    const int mode = a.paired ? 1 + (i & 1) : 0;
+    const uint32_t first = (blockIdx.x & 1) ? kSliceBytes : 0;  // line offset of the pair's first tile
+    // odd tiles of a pair read the partner half-group's schedule (its rows, their slice s+1)
+    const uint32_t hsel = (mode == 2 ? half_id ^ 1 : half_id) * 16;
     const uint32_t sbase = smem_base + b * buf_bytes + lane4 * 16;  // this lane's 16 B of tile row 0
-    uint32_t hp = head0, cp = cont0;
+    uint32_t hp = head_b + hsel, cp = cont_b + hsel;
     uint4 h0 = lds128(hp);
     long long t_wait0 = 0;
     if (a.debug & 2) t_wait0 = clock64();
     mbar_wait_backoff(smem_u32(&ready[b]), ph, a.wait_ns);
     mbar_wait(smem_u32(&full[b]), ph);
     if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2], static_cast<unsigned long long>(clock64() - t_wait0));
-    uint8_t *out = a.coded + stripe * a.coded_stride + static_cast<uint64_t>(slice) * kSliceBytes + lane4 * 16;
+    // unpaired: this slice's 64 B; paired: the pair's 128-B line (slice s = the even one)
+    uint8_t *out = a.coded + stripe * a.coded_stride +
+                   static_cast<uint64_t>(mode ? (slice & ~1u) : slice) * kSliceBytes + lane4 * 16;
     // items, with the next head chunk in flight (2-way unrolled so no register moves)
     for (uint32_t it = 0; it < nitems; it += 2) {
       const uint4 h1 = lds128(hp + kChunkBytes);
-      lt_item(h0, cp, sbase, out, a.t, half_id);
+      lt_item(h0, cp, sbase, out, a.t, half_id, tcol0 + 4 * it, mode, first);
       if (it + 1 >= nitems) break;
       h0 = lds128(hp + 2 * kChunkBytes);
       hp += 2 * kChunkBytes;
-      lt_item(h1, cp, sbase, out, a.t, half_id);
+      lt_item(h1, cp, sbase, out, a.t, half_id, tcol0 + 4 * (it + 1), mode, first);
     }
+    if (mode == 1) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // parked before reuse
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[b]));
   }
   if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2 + 1], static_cast<unsigned long long>(clock64() - t_start));
+  if (a.paired) {  // all consumer warps are done with TMEM; warp 0 frees it
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    consumer_bar();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(a.tmem_cols)
+                   : "memory");
+  }
 }
 
 // ========================================================================= GLOBAL kernels
@@ -605,7 +698,7 @@ fs_status upload_graph(Graph &g) {
   if (g.smem_eligible) {
     // two tile buffers + the schedule + the precode member rows + 6 mbarriers
     const uint64_t bytes = 2ull * g.sched.tile_units * kUnitBytes + g.sched.words.size() * 4 +
-                           ((g.sched.pre_slots.size() * 2 + 15) & ~15ull) + 6 * 8;
+                           ((g.sched.pre_slots.size() * 2 + 15) & ~15ull) + 7 * 8;
     g.smem_bytes = static_cast<uint32_t>(bytes);
     if (bytes > static_cast<uint64_t>(g.smem_optin)) {
       g.smem_eligible = false;
@@ -681,6 +774,24 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     a.data_units = g.sched.data_units;
     a.tile_units = g.sched.tile_units;
     a.sched_chunks = static_cast<uint32_t>(g.sched.words.size() / (kChunkBytes / 4));
+    // paired tiles (adjacent 64-B slices of a stripe back to back, rows leave as full 128-B lines
+    // via TMEM): even slice count and start, and the warps' TMEM column blocks fit one lane quarter
+    {
+      static const int paired_env = [] {
+        const char *e = std::getenv("FSB_PAIRED");
+        return e ? std::atoi(e) : 1;
+      }();
+      uint32_t need = 0;
+      for (int q = 0; q < 4; ++q) {
+        uint32_t c = 0;
+        for (int w = q; w < kConsumerWarps; w += 4) c += 4 * g.sched.warp_info[w * 3 + 0];
+        need = std::max(need, c);
+      }
+      uint32_t cols = 32;
+      while (cols < need) cols <<= 1;
+      a.paired = paired_env && nslices % 2 == 0 && slice0 % 2 == 0 && cols <= 512;
+      a.tmem_cols = cols;
+    }
     a.cont_base = g.sched.cont_base;
     {
       static const uint32_t dbg = [] {
@@ -694,7 +805,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
       }();
       a.wait_ns = wns;
     }
-    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, g.sm_count));
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(a.paired ? tiles / 2 : tiles, g.sm_count));
     fsb_smem_encode<<<grid, kThreads, g.smem_bytes, stream>>>(tmap, a);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_smem_encode launch");
     *launches = 1;
