@@ -16,7 +16,7 @@ if [ -f tools/microbench/mb.cu ]; then
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb tools/microbench/mb.cu && timeout 120 /tmp/mb > $OUT/microbench.txt 2>&1
 fi
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; cat $OUT/bench.json
-for c in 5 3 2; do
+for c in 5 6 7 3 2; do
   timeout 300 python bench.py --config $c --no-cpu --steps 200 > $OUT/bench_c$c.json 2> $OUT/bench_c$c.err; cat $OUT/bench_c$c.json
 done
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 0"
@@ -24,3 +24,7 @@ $CMD > $OUT/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" -c 400 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:fsb_ -s 3 -c 1 -o $OUT/prof_c4 $CMD > $OUT/ncu_full.log 2>&1
 echo "ncu rc=$?"
+for op in decode repair update; do
+  timeout 300 python bench.py --op $op --steps 200 > $OUT/bench_$op.json 2> $OUT/bench_$op.err; cat $OUT/bench_$op.json
+done
+python tools/gpu/partition_share.py 5 200 > $OUT/partition_share.json 2>&1
