@@ -441,12 +441,14 @@ def run_decode(args, cfg):
     clocks = ClockSampler(0)
     clocks.start()
     time.sleep(0.3)
+    torch.cuda.nvtx.range_push("timed")
     with torch.cuda.stream(stream):
         evs[0].record(stream)
         for i in range(args.steps):
             plan.decode(cod, inter, stream=stream)
             evs[i + 1].record(stream)
     stream.synchronize()
+    torch.cuda.nvtx.range_pop()
     clk = clocks.stop()
     ms = evs[0].elapsed_time(evs[-1]) / args.steps
     rec_bytes = S * inf["recovered_data"] * t
@@ -518,12 +520,14 @@ def run_repair(args, cfg):
     clocks = ClockSampler(0)
     clocks.start()
     time.sleep(0.3)
+    torch.cuda.nvtx.range_push("timed")
     with torch.cuda.stream(stream):
         evs[0].record(stream)
         for i in range(args.steps):
             plan.repair(cod, stream=stream)
             evs[i + 1].record(stream)
     stream.synchronize()
+    torch.cuda.nvtx.range_pop()
     clk = clocks.stop()
     ms = evs[0].elapsed_time(evs[-1]) / args.steps
     rows = len(rebuilt)

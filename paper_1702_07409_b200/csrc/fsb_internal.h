@@ -1,6 +1,7 @@
 // Internal declarations of libfsb200 (not part of the C ABI).
 #pragma once
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -147,6 +148,9 @@ struct DecodePlan {
   int32_t *d_target = nullptr, *d_src_ptr = nullptr;
   uint32_t *d_src = nullptr;
   int sm_count = 0;
+  // the level launches captured once as a CUDA graph per (S, buffers, strides) and replayed
+  // (fsb_kernels.cu; created by upload_decode_plan, guarded by its own mutex)
+  std::shared_ptr<struct PlanGraphCache> gcache;
 };
 fs_status build_decode_plan(const Graph &g, const uint8_t *received, DecodePlan &pl);
 fs_status upload_decode_plan(DecodePlan &pl);
