@@ -825,10 +825,15 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
   const uint32_t nrows = row_end - row_begin;
   if (nrows) {
     const uint32_t nbands = static_cast<uint32_t>((col_end - col_begin + kBandBytes - 1) / kBandBytes);
-    // rows per warp: up to kBandRowsMax, fewer if that leaves fewer than ~64 warps per SM
+    // rows per warp: up to kBandRowsMax (FSB_BAND_ROWS overrides: tuning experiments), fewer if
+    // that leaves fewer than ~64 warps per SM
+    static const uint32_t band_rows_max = [] {
+      const char *e = std::getenv("FSB_BAND_ROWS");
+      return e ? static_cast<uint32_t>(std::atoi(e)) : kBandRowsMax;
+    }();
     const uint64_t row_bands = static_cast<uint64_t>(S) * nbands * nrows;
     const uint32_t band_rows = static_cast<uint32_t>(
-        std::max<uint64_t>(1, std::min<uint64_t>(kBandRowsMax, row_bands / (64ull * g.sm_count))));
+        std::max<uint64_t>(1, std::min<uint64_t>(band_rows_max, row_bands / (64ull * g.sm_count))));
     const uint64_t units = static_cast<uint64_t>(S) * nbands * ((nrows + band_rows - 1) / band_rows);
     const uint64_t blocks = (units + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
     if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
