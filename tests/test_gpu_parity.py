@@ -406,3 +406,21 @@ def test_bit_probe_full_scale(cid):
             if csup[i]:
                 want[list(csup[i])] = 1
             assert np.array_equal(cb[i], want), "check %d" % i
+
+
+@pytest.mark.parametrize("t,S", [(128, 300), (192, 200), (4160, 20), (64, 400)])
+def test_smem_paired_and_unpaired_tiles(t, S):
+    """SMEM kernel with an even slice count (paired tiles: rows leave as full 128-B lines through
+    TMEM) and odd slice counts (unpaired 64-B stores), many tiles per CTA so both tile orders
+    (odd CTAs run their pairs reversed) and the TMEM column blocks of every warp are exercised."""
+    _need_gpu()
+    cfg = dict(configs.get(4), t=t, stripes=S)
+    g = fsb.Graph.create(cfg)
+    assert g.info()["smem_eligible"]
+    g.set_variant(fsb.VARIANT_SMEM)
+    D = inputs.stripe_data(cfg).numpy()
+    go = oracle.generate_graph(cfg)
+    C, Y = oracle.encode(go, D)
+    _, c, y = _run(cfg, fsb.VARIANT_SMEM, data=torch.from_numpy(D).cuda())
+    _assert_equal(c, C, "checks t=%d" % t)
+    _assert_equal(y, Y, "coded t=%d" % t)
