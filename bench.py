@@ -235,6 +235,8 @@ def main():
                          "file from the original check data (NEXT-3)")
     ap.add_argument("--erase-frac", type=float, default=0.01,
                     help="repair: fraction of coded symbols erased (seeded random subset)")
+    ap.add_argument("--eliminate", action="store_true",
+                    help="decode: finish with GF(2) elimination of the residual (FS_DECODE_ELIMINATE)")
     ap.add_argument("--recv-frac", type=float, default=0.95,
                     help="decode: fraction of coded symbols received (seeded random subset)")
     args = ap.parse_args()
@@ -425,7 +427,7 @@ def run_decode(args, cfg):
     cod = torch.empty((S, n, t), dtype=torch.uint8, device=dev)
     g.encode_stripes(data, chk, cod)
     recv = np.random.default_rng(cfg["seed"]).random(n) < args.recv_frac
-    plan = fsb.DecodePlan(g, recv)
+    plan = fsb.DecodePlan(g, recv, eliminate=args.eliminate)
     inf = plan.info()
     cod[:, torch.from_numpy(~recv).to(dev)] = 0                 # erased symbols
     inter = torch.zeros((S, K, t), dtype=torch.uint8, device=dev)
@@ -462,6 +464,7 @@ def run_decode(args, cfg):
            "config": {"workload": cfg["name"], "k": k, "p": p, "n": n, "t": t, "stripes": S,
                       "recv_frac": args.recv_frac, "received": int(recv.sum()),
                       "recovered_data": inf["recovered_data"], "levels": inf["levels"],
+                      "eliminated": inf["eliminated"], "elimination": bool(args.eliminate),
                       "xor_sources": inf["xor_sources"]},
            "roofline": {"bound": "hbm", "achieved": round(b_hbm / (ms * 1e-3) / 1e9, 1), "peak": peak,
                         "unit": "GB/s", "frac": round(b_hbm / (ms * 1e-3) / 1e9 / peak, 4),

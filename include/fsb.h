@@ -212,15 +212,26 @@ typedef struct {
   uint32_t rows;             /* rows of the plan (= recovered)                                  */
   uint32_t max_level_rows;   /* largest level                                                   */
   uint64_t xor_sources;      /* total sources over all rows (XOR work per byte column)          */
+  uint32_t eliminated;       /* symbols of the final GF(2)-elimination level (FS_DECODE_ELIMINATE) */
+  uint32_t elim_skipped;     /* 1 if the residual was too large to eliminate (> 2^28 bits)      */
 } fs_decode_info;
+
+/* fs_decode_plan_create flag: after peeling, solve the residual system (received LT rows and
+ * precode checks over the unrecovered symbols) by GF(2) Gauss-Jordan elimination on the host and
+ * add one final level that recovers every symbol the received set determines (state 2), each as
+ * the XOR of received coded rows and peeled symbols.  Not in the paper (its decoder is BP only,
+ * PAPER.md:113-134); SURVEY.md §8(f) NEXT-1's "GF(2) fallback".                               */
+#define FS_DECODE_ELIMINATE 2u
 
 /* Build the plan for graph g and the received set: received[j] != 0 iff coded symbol j is
  * available (n bytes, host).  flags: FS_GRAPH_HOST_ONLY = no device copy (fs_decode then
- * returns FS_EUNSUPPORTED).  FS_EINVAL on NULL arguments.                                   */
+ * returns FS_EUNSUPPORTED); FS_DECODE_ELIMINATE = finish with GF(2) elimination (above).
+ * FS_EINVAL on NULL arguments or unknown flags.                                             */
 FSB_API fs_status fs_decode_plan_create(const fs_graph *g, const uint8_t *received, uint32_t flags,
                                         fs_decode_plan **out);
 FSB_API fs_status fs_decode_plan_info(const fs_decode_plan *plan, fs_decode_info *info);
-/* Host views owned by the plan: state[K] (1 = recovered), level_of[K] (level, -1). */
+/* Host views owned by the plan: state[K] (1 = recovered by peeling, 2 = by elimination,
+ * 0 = not recovered), level_of[K] (level, -1). */
 FSB_API fs_status fs_decode_plan_state(const fs_decode_plan *plan, const uint8_t **state,
                                        const int32_t **level_of);
 /* Run the plan on num_stripes stripes: d_coded = coded symbols (row j at d_coded + s*coded_stride

@@ -259,11 +259,12 @@ fs_status fs_decode_plan_create(const fs_graph *h, const uint8_t *received, uint
   fsb::set_error("");
   if (!h || !received || !out) { set_error("null argument"); return FS_EINVAL; }
   *out = nullptr;
+  if (flags & ~(FS_GRAPH_HOST_ONLY | FS_DECODE_ELIMINATE)) { set_error("unknown decode flags"); return FS_EINVAL; }
   fs_decode_plan *d = new (std::nothrow) fs_decode_plan();
   if (!d) { set_error("out of host memory"); return FS_ENOMEM; }
   fs_status st;
   try {
-    st = fsb::build_decode_plan(h->g, received, d->pl);
+    st = fsb::build_decode_plan(h->g, received, d->pl, (flags & FS_DECODE_ELIMINATE) != 0);
   } catch (const std::bad_alloc &) {
     st = FS_ENOMEM;
     set_error("out of host memory");
@@ -288,12 +289,14 @@ fs_status fs_decode_plan_info(const fs_decode_plan *d, fs_decode_info *info) {
   info->levels = static_cast<uint32_t>(pl.level_ptr.size() - 1);
   info->rows = static_cast<uint32_t>(pl.target.size());
   for (uint32_t m = 0; m < pl.K; ++m) {
-    info->recovered += pl.state[m];
-    if (m < pl.k) info->recovered_data += pl.state[m];
+    info->recovered += pl.state[m] ? 1 : 0;
+    if (m < pl.k) info->recovered_data += pl.state[m] ? 1 : 0;
   }
   for (size_t L = 0; L + 1 < pl.level_ptr.size(); ++L)
     info->max_level_rows = std::max<uint32_t>(info->max_level_rows, pl.level_ptr[L + 1] - pl.level_ptr[L]);
   info->xor_sources = pl.src.size();
+  info->eliminated = pl.eliminated;
+  info->elim_skipped = pl.elim_skipped;
   return FS_OK;
 }
 

@@ -14,7 +14,136 @@
 
 namespace fsb {
 
-fs_status build_decode_plan(const Graph &g, const uint8_t *received, DecodePlan &pl) {
+namespace {
+
+// Equation e's members: LT row e (e < n) or precode check e-n with its check symbol k+(e-n).
+struct Members {
+  const Graph &g;
+  template <typename F>
+  void operator()(uint32_t e, F &&fn) const {
+    const uint32_t n = g.prm.n, k = g.prm.k;
+    if (e < n) {
+      for (int32_t x = g.lt_row_ptr[e]; x < g.lt_row_ptr[e + 1]; ++x) fn(static_cast<uint32_t>(g.lt_col[x]));
+    } else {
+      const uint32_t i = e - n;
+      for (int32_t x = g.pre_row_ptr[i]; x < g.pre_row_ptr[i + 1]; ++x) fn(static_cast<uint32_t>(g.pre_col[x]));
+      fn(k + i);
+    }
+  }
+};
+Members members_fn(const Graph &g) { return Members{g}; }
+
+// Residual GF(2) elimination after peeling ("needs an inactivation / GF(2)
+// fallback at these overheads"; not in the paper, whose decoder is BP only).  The residual system:
+// every received LT row and every precode check that still has an unknown, over the unknown
+// symbols, each row augmented with its own equation index.  Gauss-Jordan to reduced row echelon
+// form; a row whose unknown part is a unit vector e_c determines c (exactly the symbols in the
+// row space, as the oracle's elimination), as the XOR of the equations in its augmented part:
+// c = XOR over those e of (Y_e if an LT row) and of every known member, mod 2.  These rows form one
+// final level (their sources are received rows and symbols recovered by peeling).
+fs_status eliminate_residual(const Graph &g, const uint8_t *received, DecodePlan &pl, const Members &members) {
+  const uint32_t n = g.prm.n, p = g.prm.p, K = g.prm.k + p;
+  std::vector<int32_t> col_of(K, -1);
+  std::vector<uint32_t> unk;
+  for (uint32_t m = 0; m < K; ++m)
+    if (!pl.state[m]) col_of[m] = static_cast<int32_t>(unk.size()), unk.push_back(m);
+  const uint32_t u = static_cast<uint32_t>(unk.size());
+  if (!u) return FS_OK;
+  std::vector<uint32_t> eqs;
+  for (uint32_t e = 0; e < n + p; ++e) {
+    if (e < n && !received[e]) continue;
+    bool any = false;
+    members(e, [&](uint32_t m) { any = any || !pl.state[m]; });
+    if (any) eqs.push_back(e);
+  }
+  const uint32_t q = static_cast<uint32_t>(eqs.size());
+  if (static_cast<uint64_t>(u) * q > (1ull << 28)) {  // ~32 MB of bits: leave the residual
+    pl.elim_skipped = 1;
+    return FS_OK;
+  }
+  const uint32_t W1 = (u + 63) / 64, W2 = (q + 63) / 64, W = W1 + W2;
+  std::vector<uint64_t> M(static_cast<size_t>(q) * W, 0);
+  for (uint32_t r = 0; r < q; ++r) {
+    uint64_t *row = &M[static_cast<size_t>(r) * W];
+    members(eqs[r], [&](uint32_t m) {
+      if (!pl.state[m]) row[col_of[m] >> 6] ^= 1ull << (col_of[m] & 63);
+    });
+    row[W1 + (r >> 6)] |= 1ull << (r & 63);
+  }
+  uint32_t piv = 0;
+  std::vector<int32_t> pivcol;
+  for (uint32_t c = 0; c < u && piv < q; ++c) {
+    const uint32_t w = c >> 6;
+    const uint64_t bit = 1ull << (c & 63);
+    uint32_t r = piv;
+    while (r < q && !(M[static_cast<size_t>(r) * W + w] & bit)) ++r;
+    if (r == q) continue;
+    if (r != piv)
+      std::swap_ranges(M.begin() + static_cast<size_t>(r) * W, M.begin() + static_cast<size_t>(r + 1) * W,
+                       M.begin() + static_cast<size_t>(piv) * W);
+    const uint64_t *pr = &M[static_cast<size_t>(piv) * W];
+    for (uint32_t o = 0; o < q; ++o) {
+      if (o == piv) continue;
+      uint64_t *ro = &M[static_cast<size_t>(o) * W];
+      if (ro[w] & bit)
+        for (uint32_t x = w; x < W; ++x) ro[x] ^= pr[x];  // words below w are zero in the pivot row
+    }
+    pivcol.push_back(static_cast<int32_t>(c));
+    ++piv;
+  }
+  // rows whose unknown part is exactly e_c
+  std::vector<uint8_t> parity(K, 0);
+  std::vector<uint32_t> touched;
+  int32_t any_recv = -1;
+  for (uint32_t j = 0; j < n && any_recv < 0; ++j)
+    if (received[j]) any_recv = static_cast<int32_t>(j);
+  const size_t rows_before = pl.target.size();
+  for (uint32_t r = 0; r < piv; ++r) {
+    const uint64_t *row = &M[static_cast<size_t>(r) * W];
+    uint32_t pop = 0;
+    for (uint32_t x = 0; x < W1 && pop < 2; ++x) pop += static_cast<uint32_t>(__builtin_popcountll(row[x]));
+    if (pop != 1) continue;
+    const uint32_t c = unk[pivcol[r]];
+    pl.target.push_back(static_cast<int32_t>(c));
+    const size_t s0 = pl.src.size();
+    for (uint32_t x = 0; x < W2; ++x)
+      for (uint64_t bits = row[W1 + x]; bits; bits &= bits - 1) {
+        const uint32_t e = eqs[x * 64 + static_cast<uint32_t>(__builtin_ctzll(bits))];
+        if (e < n) pl.src.push_back(e | kSrcCoded);
+        members(e, [&](uint32_t m) {
+          if (pl.state[m] == 1) {
+            if (!parity[m]) touched.push_back(m);
+            parity[m] ^= 1;
+          }
+        });
+      }
+    for (uint32_t m : touched) {
+      if (parity[m]) pl.src.push_back(m);
+      parity[m] = 0;
+    }
+    touched.clear();
+    if (pl.src.size() == s0) {  // identically zero: XOR one received row with itself
+      pl.src.push_back(static_cast<uint32_t>(any_recv) | kSrcCoded);
+      pl.src.push_back(static_cast<uint32_t>(any_recv) | kSrcCoded);
+    }
+    pl.src.back() |= kSrcLast;
+    pl.src_ptr.push_back(static_cast<int32_t>(pl.src.size()));
+  }
+  if (pl.target.size() > rows_before) {
+    const int32_t L = static_cast<int32_t>(pl.level_ptr.size()) - 1;
+    for (size_t r = rows_before; r < pl.target.size(); ++r) {
+      pl.state[pl.target[r]] = 2;
+      pl.level_of[pl.target[r]] = L;
+    }
+    pl.level_ptr.push_back(static_cast<uint32_t>(pl.target.size()));
+    pl.eliminated = static_cast<uint32_t>(pl.target.size() - rows_before);
+  }
+  return FS_OK;
+}
+
+}  // namespace
+
+fs_status build_decode_plan(const Graph &g, const uint8_t *received, DecodePlan &pl, bool eliminate) {
   const uint32_t k = g.prm.k, p = g.prm.p, n = g.prm.n, K = k + p;
   pl = DecodePlan();
   pl.k = k, pl.p = p, pl.n = n, pl.K = K, pl.t = g.prm.t;
@@ -102,6 +231,7 @@ fs_status build_decode_plan(const Graph &g, const uint8_t *received, DecodePlan 
     next.erase(std::unique(next.begin(), next.end()), next.end());
     cand.swap(next);
   }
+  if (eliminate) return eliminate_residual(g, received, pl, members_fn(g));
   return FS_OK;
 }
 

@@ -144,6 +144,8 @@ struct DecodePlan {
   std::vector<uint32_t> src;         // flagged source list
   std::vector<uint8_t> state;        // K: 1 recovered, 0 not
   std::vector<int32_t> level_of;     // K: level that recovered it, -1
+  uint32_t eliminated = 0;           // symbols of the final residual-elimination level
+  uint32_t elim_skipped = 0;         // 1: residual too large, elimination not attempted
   int device = -1;
   int32_t *d_target = nullptr, *d_src_ptr = nullptr;
   uint32_t *d_src = nullptr;
@@ -152,7 +154,7 @@ struct DecodePlan {
   // (fsb_kernels.cu; created by upload_decode_plan, guarded by its own mutex)
   std::shared_ptr<struct PlanGraphCache> gcache;
 };
-fs_status build_decode_plan(const Graph &g, const uint8_t *received, DecodePlan &pl);
+fs_status build_decode_plan(const Graph &g, const uint8_t *received, DecodePlan &pl, bool eliminate);
 fs_status upload_decode_plan(DecodePlan &pl);
 void free_decode_plan(DecodePlan &pl);
 fs_status launch_decode(const DecodePlan &pl, uint32_t S, const uint8_t *coded, uint64_t coded_stride,

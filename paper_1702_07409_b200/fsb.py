@@ -16,6 +16,7 @@ FS_OK, FS_EINVAL, FS_EDIST, FS_ENOMEM, FS_ECUDA, FS_EUNSUPPORTED = 0, -1, -2, -3
 FS_DIST_RSD, FS_DIST_FINITE = 1, 2
 FS_PRECODE_RANDOM, FS_PRECODE_ARRAY = 0, 1
 FS_GRAPH_HOST_ONLY = 1
+FS_DECODE_ELIMINATE = 2
 VARIANT_AUTO, VARIANT_SMEM, VARIANT_GLOBAL = 0, 1, 2
 
 # Every symbol include/fsb.h declares (checked by tests/test_capi.py).
@@ -70,7 +71,8 @@ class fs_decode_info(ctypes.Structure):
     _fields_ = [("K", ctypes.c_uint32), ("n", ctypes.c_uint32), ("received", ctypes.c_uint32),
                 ("recovered", ctypes.c_uint32), ("recovered_data", ctypes.c_uint32),
                 ("levels", ctypes.c_uint32), ("rows", ctypes.c_uint32),
-                ("max_level_rows", ctypes.c_uint32), ("xor_sources", ctypes.c_uint64)]
+                ("max_level_rows", ctypes.c_uint32), ("xor_sources", ctypes.c_uint64),
+                ("eliminated", ctypes.c_uint32), ("elim_skipped", ctypes.c_uint32)]
 
 
 _lib = None
@@ -301,15 +303,15 @@ class Graph:
 class DecodePlan:
     """Owner of an fs_decode_plan: Alg 5 (DPG) levels for a graph and a received set."""
 
-    def __init__(self, graph, received, host_only=False):
+    def __init__(self, graph, received, host_only=False, eliminate=False):
         rv = np.ascontiguousarray(np.asarray(received, dtype=bool).astype(np.uint8))
         if rv.shape != (graph.n,):
             raise ValueError("received must have n entries")
         self.graph = graph
         self._h = None
         h = ctypes.c_void_p()
-        _check(lib().fs_decode_plan_create(graph._h, rv.ctypes.data_as(ctypes.c_void_p),
-                                           FS_GRAPH_HOST_ONLY if host_only else 0, ctypes.byref(h)))
+        flags = (FS_GRAPH_HOST_ONLY if host_only else 0) | (FS_DECODE_ELIMINATE if eliminate else 0)
+        _check(lib().fs_decode_plan_create(graph._h, rv.ctypes.data_as(ctypes.c_void_p), flags, ctypes.byref(h)))
         self._h = h
 
     def info(self):

@@ -127,6 +127,27 @@ def test_gpu_decode_matches_oracle(cid, frac, S):
             assert np.array_equal(I[s][c["k"]:][chk_rec], C[s][chk_rec])
 
 
+@pytest.mark.parametrize("cid,frac", [(1, 1.0), (1, 0.97), (2, 0.95), (3, 0.98), (4, 1.0), (4, 0.9)])
+def test_plan_elimination_matches_oracle(cid, frac):
+    """FS_DECODE_ELIMINATE: the plan recovers exactly the symbols the received equations determine
+    (the oracle's BP + Gauss-Jordan state: 1 = peeled, 2 = eliminated), every peeled one in the
+    same way as without elimination."""
+    c = _small(cid)
+    recv = _recv(c["n"], frac, 11 + cid)
+    go = oracle.generate_graph(c)
+    g = fsb.Graph.create(c, host_only=True)
+    D = inputs.stripe_data(c).numpy()[0]
+    _, Y = oracle.encode(go, D)
+    _, ostate = oracle.decode(go, recv, Y, use_elim=True)
+    plan = fsb.DecodePlan(g, recv, host_only=True, eliminate=True)
+    st, lev = plan.state()
+    assert np.array_equal(st, ostate)
+    inf = plan.info()
+    assert inf["eliminated"] == int((ostate == 2).sum()) and not inf["elim_skipped"]
+    base = fsb.DecodePlan(g, recv, host_only=True).state()
+    assert np.array_equal(base[0], (st == 1).astype(base[0].dtype)) and np.array_equal(base[1][st == 1], lev[st == 1])
+
+
 def test_plan_with_array_precode_matches_oracle():
     """Decoding through Alg 2 checks (checks whose members include earlier checks)."""
     c = dict(configs.get(6), n=1150)
@@ -138,3 +159,34 @@ def test_plan_with_array_precode_matches_oracle():
     _, Y = oracle.encode(go, D)
     _, ostate = oracle.decode(go, recv, Y, use_elim=False)
     assert np.array_equal(st, (ostate == 1).astype(np.uint8))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cid,frac,S", [(1, 0.97, 3), (4, 1.0, 2), (4, 0.9, 2), (3, 0.98, 1)])
+def test_gpu_decode_eliminate_matches_oracle(cid, frac, S):
+    """GPU bytes of the peeling levels + the elimination level = the oracle's BP + Gauss-Jordan
+    decode, = the source data for every determined data symbol."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = dict(_small(cid), stripes=S)
+    recv = _recv(c["n"], frac, 11 + cid)
+    go = oracle.generate_graph(c)
+    D = inputs.stripe_data(c).numpy()
+    C, Y = oracle.encode(go, D)
+    g = fsb.Graph.create(c)
+    plan = fsb.DecodePlan(g, recv, eliminate=True)
+    K, t = c["k"] + c["p"], c["t"]
+    Yd = torch.from_numpy(Y).cuda()
+    Yd[:, ~torch.from_numpy(recv)] = 0x77
+    inter = torch.full((S, K, t), 0xA5, dtype=torch.uint8, device="cuda")
+    plan.decode(Yd, inter)
+    torch.cuda.synchronize()
+    I = inter.cpu().numpy()
+    st, _ = plan.state()
+    for s in range(S):
+        oI, ostate = oracle.decode(go, recv, Y[s], use_elim=True)
+        rec = ostate != 0
+        assert np.array_equal(st != 0, rec)
+        assert np.array_equal(I[s][rec], oI[rec])
+        assert np.all(I[s][~rec] == 0xA5)
+        assert np.array_equal(I[s][:c["k"]][rec[:c["k"]]], D[s][rec[:c["k"]]])
