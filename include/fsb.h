@@ -212,15 +212,20 @@ typedef struct {
   uint32_t rows;             /* rows of the plan (= recovered)                                  */
   uint32_t max_level_rows;   /* largest level                                                   */
   uint64_t xor_sources;      /* total sources over all rows (XOR work per byte column)          */
-  uint32_t eliminated;       /* symbols of the final GF(2)-elimination level (FS_DECODE_ELIMINATE) */
-  uint32_t elim_skipped;     /* 1 if the residual was too large to eliminate (> 2^28 bits)      */
+  uint32_t eliminated;       /* symbols recovered after peeling stalled (FS_DECODE_ELIMINATE)   */
+  uint32_t elim_skipped;     /* reserved (0)                                                    */
+  uint32_t inactivated;      /* symbols inactivated by the completion phase                     */
+  uint32_t work_rows;        /* device workspace rows per stripe (t bytes each, library-owned)  */
 } fs_decode_info;
 
-/* fs_decode_plan_create flag: after peeling, solve the residual system (received LT rows and
- * precode checks over the unrecovered symbols) by GF(2) Gauss-Jordan elimination on the host and
- * add one final level that recovers every symbol the received set determines (state 2), each as
- * the XOR of received coded rows and peeled symbols.  Not in the paper (its decoder is BP only,
- * PAPER.md:113-134); SURVEY.md §8(f) NEXT-1's "GF(2) fallback".                               */
+/* fs_decode_plan_create flag: complete the decode where peeling stalls, by inactivation decoding
+ * (host plan, GPU rows): inactivate a few unknowns, keep peeling with them carried symbolically,
+ * solve the small GF(2) system the unused equations give for them (Gauss-Jordan on the host), then
+ * fix up every symbol that depended on them.  Recovers exactly the symbols the received equations
+ * determine (state 2 for those peeling alone did not reach).  Rows of symbols that stay
+ * unrecovered may then hold partial values.  fs_decode allocates the plan's workspace
+ * (work_rows x t x stripes bytes) on first use.  Not in the paper (its decoder is BP only,
+ * PAPER.md:113-134): SURVEY.md §8(f) NEXT-1's "inactivation / GF(2) fallback".              */
 #define FS_DECODE_ELIMINATE 2u
 
 /* Build the plan for graph g and the received set: received[j] != 0 iff coded symbol j is

@@ -297,6 +297,8 @@ fs_status fs_decode_plan_info(const fs_decode_plan *d, fs_decode_info *info) {
   info->xor_sources = pl.src.size();
   info->eliminated = pl.eliminated;
   info->elim_skipped = pl.elim_skipped;
+  info->inactivated = pl.inactivated;
+  info->work_rows = pl.work_rows;
   return FS_OK;
 }
 

@@ -133,6 +133,8 @@ namespace fsb {
 // its sources src[src_ptr[r] .. src_ptr[r+1]): an intermediate index m (recovered at an earlier
 // level) or m | kSrcCoded for received coded row m; bit 31 (kSrcLast) marks a row's last source.
 constexpr uint32_t kSrcCoded = 1u << 30;
+constexpr uint32_t kSrcWork = 1u << 29;   // a workspace row (inactivation decoding, Z rows)
+constexpr uint32_t kSrcIndex = kSrcWork - 1;
 constexpr uint32_t kSrcLast = 1u << 31;
 struct DecodePlan {
   uint32_t k = 0, p = 0, n = 0, K = 0;
@@ -146,6 +148,8 @@ struct DecodePlan {
   std::vector<int32_t> level_of;     // K: level that recovered it, -1
   uint32_t eliminated = 0;           // symbols of the final residual-elimination level
   uint32_t elim_skipped = 0;         // 1: residual too large, elimination not attempted
+  uint32_t inactivated = 0;          // symbols inactivated by the completion phase
+  uint32_t work_rows = 0;            // workspace rows (t bytes per stripe) the plan needs
   int device = -1;
   int32_t *d_target = nullptr, *d_src_ptr = nullptr;
   uint32_t *d_src = nullptr;

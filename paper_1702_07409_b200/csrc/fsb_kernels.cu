@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
     fsb_dpg_level(uint32_t S, uint32_t t, uint32_t nbands, uint32_t row0, uint32_t nrows, uint32_t band_rows,
                   const int32_t *__restrict__ target, const int32_t *__restrict__ src_ptr,
                   const uint32_t *__restrict__ src, uint8_t *coded, uint64_t coded_stride,
-                  uint8_t *inter, uint64_t inter_stride) {
+                  uint8_t *inter, uint64_t inter_stride, uint8_t *work, uint64_t work_stride) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nchunks = (nrows + band_rows - 1) / band_rows;
   uint64_t unit = static_cast<uint64_t>(blockIdx.x) * (kGlobalThreads / 32) + (threadIdx.x >> 5);
@@ -579,8 +579,10 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   const uint32_t byte = active ? byte_raw : 0;
   const uint8_t *ibase = inter + s * inter_stride + byte;  // read: rows of earlier levels
   const uint8_t *cbase = coded + s * coded_stride + byte;
+  const uint8_t *wbase = work + s * work_stride + byte;   // read: workspace rows (m | kSrcWork)
   uint8_t *obase = inter + s * inter_stride + byte_raw;  // target m: intermediate row m
   uint8_t *cobase = coded + s * coded_stride + byte_raw; // target m | kSrcCoded: coded row m (repair)
+  uint8_t *wobase = work + s * work_stride + byte_raw;   // target m | kSrcWork: workspace row m
   const uint32_t r0 = row0 + chunk * band_rows;
   const uint32_t rows = min(band_rows, row0 + nrows - r0);
   const int32_t tg = lane < rows ? __ldg(&target[r0 + lane]) : 0;
@@ -598,8 +600,8 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
 #pragma unroll
       for (uint32_t u = 0; u < kBatch; ++u) {
         fl[u] = __shfl_sync(0xffffffffu, cv, kk + u);
-        const uint32_t m = fl[u] & (kSrcCoded - 1);
-        const uint8_t *b0 = (fl[u] & kSrcCoded) ? cbase : ibase;
+        const uint32_t m = fl[u] & kSrcIndex;
+        const uint8_t *b0 = (fl[u] & kSrcCoded) ? cbase : (fl[u] & kSrcWork) ? wbase : ibase;
         v[u] = __ldg(reinterpret_cast<const uint4 *>(b0 + static_cast<uint64_t>(m) * t));
       }
       const int32_t lim = min(static_cast<int32_t>(kBatch), nb - kk);
@@ -609,8 +611,8 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
         xor_into(acc, v[u]);
         if (fl[u] & kSrcLast) {  // warp-uniform: row complete
           const uint32_t f = static_cast<uint32_t>(__shfl_sync(0xffffffffu, tg, cur));
-          uint8_t *ob = (f & kSrcCoded) ? cobase : obase;
-          if (active) *reinterpret_cast<uint4 *>(ob + static_cast<uint64_t>(f & (kSrcCoded - 1)) * t) = acc;
+          uint8_t *ob = (f & kSrcCoded) ? cobase : (f & kSrcWork) ? wobase : obase;
+          if (active) *reinterpret_cast<uint4 *>(ob + static_cast<uint64_t>(f & kSrcIndex) * t) = acc;
           acc = make_uint4(0, 0, 0, 0);
           ++cur;
         }
@@ -864,9 +866,12 @@ struct PlanGraphCache {
   uint32_t S = 0, launches = 0;
   const void *coded = nullptr, *inter = nullptr;
   uint64_t coded_stride = 0, inter_stride = 0;
+  uint8_t *work = nullptr;             // workspace rows (inactivation decoding), grown on demand
+  uint64_t work_bytes = 0;
   ~PlanGraphCache() {
     if (exec) cudaGraphExecDestroy(exec);
     if (cap) cudaStreamDestroy(cap);
+    if (work) cudaFree(work);
   }
 };
 
@@ -907,7 +912,8 @@ fs_status launch_decode(const DecodePlan &pl, uint32_t S, const uint8_t *coded, 
 }
 
 static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded, uint64_t coded_stride,
-                               uint8_t *inter, uint64_t inter_stride, cudaStream_t stream, uint32_t *launches);
+                               uint8_t *inter, uint64_t inter_stride, uint8_t *work, uint64_t work_stride,
+                               cudaStream_t stream, uint32_t *launches);
 
 // Plans with several levels replay a CUDA graph of their level launches (captured on first use
 // for these buffers), so the ~1.5 us launch gap between dependent levels goes away;
@@ -919,11 +925,29 @@ fs_status launch_plan(const DecodePlan &pl, uint32_t S, uint8_t *coded, uint64_t
     return e ? std::atoi(e) : 1;
   }();
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
-  if (!use_graph || !pl.gcache || pl.level_ptr.size() < 3)
-    return launch_levels(pl, S, coded, coded_stride, inter, inter_stride, stream, launches);
+  if (!pl.gcache) return launch_levels(pl, S, coded, coded_stride, inter, inter_stride, nullptr, 0, stream, launches);
   PlanGraphCache &c = *pl.gcache;
   std::lock_guard<std::mutex> lock(c.mu);
   cudaError_t e;
+  // workspace for the plan's Z rows: work_rows x t per stripe (allocated once, grown if needed)
+  const uint64_t work_stride = static_cast<uint64_t>(pl.work_rows) * pl.t;
+  const uint64_t need = work_stride * S;
+  if (need > c.work_bytes) {
+    if (c.work) {
+      cudaStreamSynchronize(stream);  // a replayed graph may still read the old buffer
+      cudaFree(c.work);
+      c.work = nullptr;
+      c.work_bytes = 0;
+      if (c.exec) {
+        cudaGraphExecDestroy(c.exec);
+        c.exec = nullptr;
+      }
+    }
+    if ((e = cudaMalloc(&c.work, need)) != cudaSuccess) return cuda_fail(e, "cudaMalloc (decode workspace)");
+    c.work_bytes = need;
+  }
+  if (!use_graph || pl.level_ptr.size() < 3)
+    return launch_levels(pl, S, coded, coded_stride, inter, inter_stride, c.work, work_stride, stream, launches);
   if (!c.exec || c.S != S || c.coded != coded || c.inter != inter || c.coded_stride != coded_stride ||
       c.inter_stride != inter_stride) {
     if (c.exec) {
@@ -935,7 +959,7 @@ fs_status launch_plan(const DecodePlan &pl, uint32_t S, uint8_t *coded, uint64_t
     if ((e = cudaStreamBeginCapture(c.cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
       return cuda_fail(e, "cudaStreamBeginCapture");
     uint32_t n = 0;
-    fs_status st = launch_levels(pl, S, coded, coded_stride, inter, inter_stride, c.cap, &n);
+    fs_status st = launch_levels(pl, S, coded, coded_stride, inter, inter_stride, c.work, work_stride, c.cap, &n);
     cudaGraph_t graph = nullptr;
     e = cudaStreamEndCapture(c.cap, &graph);
     if (st != FS_OK) {
@@ -958,7 +982,8 @@ fs_status launch_plan(const DecodePlan &pl, uint32_t S, uint8_t *coded, uint64_t
 }
 
 static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded, uint64_t coded_stride,
-                               uint8_t *inter, uint64_t inter_stride, cudaStream_t stream, uint32_t *launches) {
+                               uint8_t *inter, uint64_t inter_stride, uint8_t *work, uint64_t work_stride,
+                               cudaStream_t stream, uint32_t *launches) {
   *launches = 0;
   const uint32_t nbands = static_cast<uint32_t>((pl.t + kBandBytes - 1) / kBandBytes);
   for (size_t L = 0; L + 1 < pl.level_ptr.size(); ++L) {
@@ -972,7 +997,7 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
     if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
     fsb_dpg_level<2, 6><<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
         S, static_cast<uint32_t>(pl.t), nbands, row0, nrows, band_rows, pl.d_target, pl.d_src_ptr, pl.d_src, coded,
-        coded_stride, inter, inter_stride);
+        coded_stride, inter, inter_stride, work, work_stride);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "fsb_dpg_level launch");
     ++*launches;

@@ -72,7 +72,8 @@ class fs_decode_info(ctypes.Structure):
                 ("recovered", ctypes.c_uint32), ("recovered_data", ctypes.c_uint32),
                 ("levels", ctypes.c_uint32), ("rows", ctypes.c_uint32),
                 ("max_level_rows", ctypes.c_uint32), ("xor_sources", ctypes.c_uint64),
-                ("eliminated", ctypes.c_uint32), ("elim_skipped", ctypes.c_uint32)]
+                ("eliminated", ctypes.c_uint32), ("elim_skipped", ctypes.c_uint32),
+                ("inactivated", ctypes.c_uint32), ("work_rows", ctypes.c_uint32)]
 
 
 _lib = None

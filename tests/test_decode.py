@@ -162,10 +162,11 @@ def test_plan_with_array_precode_matches_oracle():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cid,frac,S", [(1, 0.97, 3), (4, 1.0, 2), (4, 0.9, 2), (3, 0.98, 1)])
+@pytest.mark.parametrize("cid,frac,S", [(1, 0.97, 3), (1, 1.0, 1), (2, 0.9, 2), (4, 1.0, 2), (4, 0.9, 2),
+                                         (4, 0.82, 1), (3, 0.98, 1), (3, 0.9, 1)])
 def test_gpu_decode_eliminate_matches_oracle(cid, frac, S):
-    """GPU bytes of the peeling levels + the elimination level = the oracle's BP + Gauss-Jordan
-    decode, = the source data for every determined data symbol."""
+    """GPU bytes of the peeling levels + the inactivation-decoding rows = the oracle's BP +
+    Gauss-Jordan decode, = the source data for every determined data symbol."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     c = dict(_small(cid), stripes=S)
@@ -187,6 +188,5 @@ def test_gpu_decode_eliminate_matches_oracle(cid, frac, S):
         oI, ostate = oracle.decode(go, recv, Y[s], use_elim=True)
         rec = ostate != 0
         assert np.array_equal(st != 0, rec)
-        assert np.array_equal(I[s][rec], oI[rec])
-        assert np.all(I[s][~rec] == 0xA5)
+        assert np.array_equal(I[s][rec], oI[rec])           # (unrecovered rows may hold partials)
         assert np.array_equal(I[s][:c["k"]][rec[:c["k"]]], D[s][rec[:c["k"]]])
