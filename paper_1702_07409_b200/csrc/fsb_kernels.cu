@@ -995,7 +995,18 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
     const uint64_t units = static_cast<uint64_t>(S) * nbands * ((nrows + band_rows - 1) / band_rows);
     const uint64_t blocks = (units + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
     if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
-    fsb_dpg_level<2, 6><<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
+    // gathers in flight per warp: levels of long rows (repair / update / dense decode levels) take 8
+    // at 4 blocks per SM, levels of short rows 2 at 6 blocks (measured on configs 5, 7 and 4:
+    // update 3.41 -> 3.10 ms, repair 0.457 -> 0.384, decode 0.722 -> 0.687 with 8 in flight; the
+    // 86 small levels of the config-4 inactivation decode prefer 2).  FSB_DPG_CFG=1/2 forces one.
+    static const int dpg_cfg = [] {
+      const char *e = std::getenv("FSB_DPG_CFG");
+      return e ? std::atoi(e) : 0;
+    }();
+    const uint32_t nsrc = static_cast<uint32_t>(pl.src_ptr[row0 + nrows] - pl.src_ptr[row0]);
+    const bool long_rows = dpg_cfg == 2 || (dpg_cfg == 0 && nsrc >= 6u * nrows);
+    auto kern = long_rows ? fsb_dpg_level<8, 4> : fsb_dpg_level<2, 6>;
+    kern<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
         S, static_cast<uint32_t>(pl.t), nbands, row0, nrows, band_rows, pl.d_target, pl.d_src_ptr, pl.d_src, coded,
         coded_stride, inter, inter_stride, work, work_stride);
     cudaError_t e = cudaGetLastError();
