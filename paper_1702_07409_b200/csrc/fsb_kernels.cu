@@ -6,17 +6,17 @@
 //
 // Two variants, bit-identical output (XOR is exact and order-free):
 //
-// SMEM  (fsb_smem_encode): persistent, one CTA per SM.  A tile = (stripe, 128-byte slice of
-//       every symbol).  A TMA producer warp streams the tile's k data rows (32 rows x 128 B
-//       per cp.async.bulk.tensor box) into a shared-memory ring; 16 consumer warps compute
-//       the p checks from shared memory (written back to smem and HBM), then every coded
-//       row as a register XOR of 16-B lanes gathered from shared memory, and store it with
-//       one full 128-B line per row.  HBM sees each source byte once and each output byte
-//       once (the ideal one-read-one-write roofline); the gathers hit shared memory only.
-//       Tiles alternate between the two ends of the ring so the next tile's rows stream in
-//       while the current one computes.  Work per warp comes from a host-built, degree-
-//       aware schedule (fsb_graph.cpp): heavy rows are split over the 4 lane-groups of a
-//       warp and recombined with shuffles; light rows are packed by equal degree.
+// SMEM  (fsb_smem_encode): persistent, one CTA per SM.  A tile = (stripe, 64-byte slice of
+//       every symbol).  A TMA warp streams the tile's k data rows (64 rows x 64 B per
+//       cp.async.bulk.tensor box) into one of two tile buffers; 3 precode warps compute the p
+//       checks from shared memory (written back to smem and HBM); 24 consumer warps compute
+//       every coded row as a register XOR of 16-B lanes gathered from shared memory.  Tiles
+//       come in pairs (the two 64-B halves of a 128-B column): the first tile's row results
+//       are parked in tensor memory, the second tile stores every row as one full 128-B line.
+//       HBM sees each source byte once and each output byte once (the ideal one-read-one-write
+//       roofline); the gathers hit shared memory only.  Work per warp comes from a host-built,
+//       degree-aware schedule (fsb_graph.cpp): light rows are paired by even/odd source counts
+//       (bank rule), heavy rows split over two or eight half-groups and recombined by shuffles.
 //
 // GLOBAL (fsb_precode_global + fsb_lt_band): no staging; every group of 8 lanes XORs one
 //       (row, 128-B slice) by 16-B loads from global memory, with the launch rasterised
@@ -286,12 +286,14 @@ __device__ __forceinline__ bool tile_of(const SmemArgs &a, uint32_t i, uint32_t 
 }
 
 // Persistent encode kernel, one CTA per SM.  Shared memory: two tile buffers (tile_units x 4 KiB
-// each), the LT schedule, then the mbarriers.  Warp roles:
-//   producer warp (16): lane 0 streams each tile's data rows in by TMA (box kUnitRows x 64 B);
-//     then the whole warp computes the tile's p precode checks (PAPER.md:91 step (1)) from
-//     shared memory into the buffer's check rows and to HBM, and signals `ready`;
-//   consumer warps (0..15): every LT row (PAPER.md:91 step (2)) of the tile as a register XOR of
-//     64-B rows gathered from shared memory, one 64-B store per row.
+// each), the LT schedule, the precode member rows, then the mbarriers and the TMEM address.
+// Warp roles:
+//   TMA warp (kConsumerWarps): lane 0 streams each tile's data rows in by TMA (box kUnitRows x 64 B);
+//   precode warps (the last kPrecodeWarps): the tile's p checks (PAPER.md:91 step (1)) from shared
+//     memory into the buffer's check rows and to HBM, level by level, then `ready`;
+//   consumer warps (0..kConsumerWarps-1): every LT row (PAPER.md:91 step (2)) of the tile as a
+//     register XOR of 64-B rows gathered from shared memory (lt_item: 64-B stores unpaired,
+//     TMEM-parked halves and full 128-B lines paired).
 // Buffers alternate (tile i uses buffer i&1), so tile i+1 streams in while tile i computes, and a
 // consumer warp that finishes tile i early starts tile i+1 without waiting for the others.
 __global__ void __launch_bounds__(kThreads, 1)
