@@ -211,10 +211,13 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
   const uint32_t ctrl = h.x >> 16;
   const uint32_t L = ctrl & kMaxItemLen;
   uint4 acc = make_uint4(0, 0, 0, 0);
+  // the first continuation chunk is requested before the head gathers, so its latency overlaps
+  // them instead of following them
+  uint4 c = make_uint4(0, 0, 0, 0);
+  if (L > kHeadSlots) c = lds128(cp);
   gather_xor_n<2>(acc, h, L < kHeadSlots ? L : kHeadSlots, sbase);
   if (L > kHeadSlots) {
     uint32_t rem = L - kHeadSlots;
-    uint4 c = lds128(cp);
     cp += kChunkBytes;
     for (; rem > kChunkSlots; rem -= kChunkSlots) {
       const uint4 nx = lds128(cp);  // next chunk in flight while this one is gathered
