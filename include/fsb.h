@@ -23,9 +23,12 @@
  * (reading R13).  Data of stripe s starts at d_data + s*data_stride, etc.
  *
  * Ownership: the library owns fs_graph (host CSR, device CSR, device work schedules,
- * allocated on the device current at creation).  The caller owns every data / check /
- * coded buffer.  The library never allocates caller-visible memory and never
- * synchronises the caller's stream; kernels are enqueued on the stream given.
+ * allocated on the device current at creation) and the decode/repair plans (and, for
+ * FS_DECODE_ELIMINATE plans, their device workspace, allocated on first use).  The caller
+ * owns every data / check / coded buffer.  The library never allocates caller-visible memory
+ * and never synchronises the caller's stream (except when a plan's workspace grows);
+ * kernels are enqueued on the stream given.  Encode / decode / repair calls must be made
+ * with the object's device current (else FS_EINVAL).
  *
  * Errors: every call returns fs_status (0 = OK).  Validation failures return FS_EINVAL /
  * FS_EDIST without side effects; launch failures return FS_ECUDA.  Asynchronous kernel
@@ -34,6 +37,8 @@
  *
  * Thread safety: a graph is immutable after creation (except fs_graph_set_variant, which
  * must not race with encodes); concurrent fs_encode* calls on different streams are fine.
+ * Plans cache a CUDA graph of their level launches and their workspace under an internal
+ * mutex: concurrent fs_decode / fs_repair calls on one plan are serialised on the host.
  * Output is deterministic and independent of stream, launch configuration, kernel
  * variant and GPU count (XOR is exact, associative and commutative).
  */

@@ -728,6 +728,15 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
   *launches = 0;
   const fs_params &prm = g.prm;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != g.dev.device) {
+      set_error("the graph lives on device " + std::to_string(g.dev.device) + ", the current device is " +
+                std::to_string(cur));
+      return FS_EINVAL;
+    }
+  }
   // SMEM tiles need the column range on 64-B slice boundaries
   const bool slice_aligned = col_begin % kSliceBytes == 0 && (col_end % kSliceBytes == 0 || col_end == prm.t);
   const uint32_t slice0 = static_cast<uint32_t>(col_begin / kSliceBytes);
@@ -930,6 +939,15 @@ fs_status launch_plan(const DecodePlan &pl, uint32_t S, uint8_t *coded, uint64_t
     return e ? std::atoi(e) : 1;
   }();
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != pl.device) {
+      set_error("the plan lives on device " + std::to_string(pl.device) + ", the current device is " +
+                std::to_string(cur));
+      return FS_EINVAL;
+    }
+  }
   if (!pl.gcache) return launch_levels(pl, S, coded, coded_stride, inter, inter_stride, nullptr, 0, stream, launches);
   PlanGraphCache &c = *pl.gcache;
   std::lock_guard<std::mutex> lock(c.mu);
