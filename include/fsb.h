@@ -38,7 +38,8 @@
  * Thread safety: a graph is immutable after creation (except fs_graph_set_variant, which
  * must not race with encodes); concurrent fs_encode* calls on different streams are fine.
  * Plans cache a CUDA graph of their level launches and their workspace under an internal
- * mutex: concurrent fs_decode / fs_repair calls on one plan are serialised on the host.
+ * mutex (host calls on one plan are serialised); a plan with a workspace (FS_DECODE_ELIMINATE)
+ * must not run on two streams at once -- order such calls (one stream, or events).
  * Output is deterministic and independent of stream, launch configuration, kernel
  * variant and GPU count (XOR is exact, associative and commutative).
  */
