@@ -246,6 +246,8 @@ def main():
     if args.op in ("repair", "update") and "--config" not in sys.argv:
         args.config = 7
     cfg = configs.get(args.config)
+    if args.op != "encode" and _dist_env()[1] != 0:
+        return  # the decode / repair / update lines are single-GPU: rank 0 runs them
     if args.op == "decode":
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "decode reference arm not implemented"}))
