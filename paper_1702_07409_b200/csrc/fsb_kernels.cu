@@ -571,6 +571,11 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
                   const int32_t *__restrict__ target, const int32_t *__restrict__ src_ptr,
                   const uint32_t *__restrict__ src, uint8_t *coded, uint64_t coded_stride,
                   uint8_t *inter, uint64_t inter_stride, uint8_t *work, uint64_t work_stride) {
+  // programmatic dependent launch: this level's CTAs may be scheduled while the previous level
+  // drains; they wait here until it has completed and its writes are visible, and let the next
+  // level be scheduled as soon as every CTA of this one has started
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nchunks = (nrows + band_rows - 1) / band_rows;
   uint64_t unit = static_cast<uint64_t>(blockIdx.x) * (kGlobalThreads / 32) + (threadIdx.x >> 5);
@@ -1029,10 +1034,26 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
     const uint32_t nsrc = static_cast<uint32_t>(pl.src_ptr[row0 + nrows] - pl.src_ptr[row0]);
     const bool long_rows = dpg_cfg == 2 || (dpg_cfg == 0 && nsrc >= 6u * nrows);
     auto kern = long_rows ? fsb_dpg_level<8, 4> : fsb_dpg_level<2, 6>;
-    kern<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, static_cast<uint32_t>(pl.t), nbands, row0, nrows, band_rows, pl.d_target, pl.d_src_ptr, pl.d_src, coded,
-        coded_stride, inter, inter_stride, work, work_stride);
-    cudaError_t e = cudaGetLastError();
+    static const int use_pdl = [] {
+      const char *e = std::getenv("FSB_PDL");
+      return e ? std::atoi(e) : 1;
+    }();
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(static_cast<uint32_t>(blocks));
+    lc.blockDim = dim3(kGlobalThreads);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = use_pdl && L > 0 ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&lc, kern, S, static_cast<uint32_t>(pl.t), nbands, row0, nrows, band_rows,
+                                       static_cast<const int32_t *>(pl.d_target),
+                                       static_cast<const int32_t *>(pl.d_src_ptr),
+                                       static_cast<const uint32_t *>(pl.d_src), coded, coded_stride, inter,
+                                       inter_stride, work, work_stride);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "fsb_dpg_level launch");
     ++*launches;
   }
