@@ -471,6 +471,8 @@ __global__ void __launch_bounds__(kGlobalThreads)
     fsb_precode_global(uint32_t S, uint32_t c0, uint32_t nc, uint32_t k, uint32_t d_p, uint64_t t, uint64_t col0,
                        uint64_t col1, uint32_t nslices, const int32_t *__restrict__ pre_col, const uint8_t *__restrict__ data,
                        uint64_t data_stride, uint8_t *checks, uint64_t checks_stride) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // an earlier precode level (PDL)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint64_t item = static_cast<uint64_t>(blockIdx.x) * kGroupsPerBlock + (threadIdx.x >> 3);
   const uint32_t lane8 = threadIdx.x & 7;
   const uint64_t total = static_cast<uint64_t>(S) * nc * nslices;
@@ -517,7 +519,10 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   unit /= nchunks;
   const uint32_t band = static_cast<uint32_t>(unit % nbands);
   const uint64_t s = unit / nbands;
-  if (s >= S) return;
+  if (s >= S) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // never complete before the precode grid
+    return;
+  }
   const uint32_t byte_raw = col0 + band * kBandBytes + lane * 16;  // bands cover columns [col0, col1)
   const bool active = byte_raw < col1;                // ragged last band
   const uint32_t byte = active ? byte_raw : col0;     // inactive lanes load a valid address
@@ -530,6 +535,9 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   const int32_t end = __ldg(&row_ptr[row_begin + r0 + rows]);
   uint8_t *out = coded + s * coded_stride + static_cast<uint64_t>(r0) * t + byte_raw;
   uint4 acc = make_uint4(0, 0, 0, 0);
+  // launched programmatically after the precode kernel (PDL): rows run while the checks are
+  // still being computed; a warp waits for the precode grid only before its first check source
+  bool checks_ready = false;
   for (int32_t e0 = base; e0 < end; e0 += 32) {
     // 32 marked column indices (bit 31 = last edge of its row) per coalesced load; positions
     // past `end` read row 0 and are never XORed
@@ -542,6 +550,10 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
       for (uint32_t u = 0; u < kBandBatch; ++u) {
         mr[u] = __shfl_sync(0xffffffffu, cv, kk + u);
         const uint32_t m = mr[u] & 0x7FFFFFFFu;
+        if (m >= k && !checks_ready) {  // warp-uniform: the precode launch must have completed
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          checks_ready = true;
+        }
         const uint8_t *b0 = m < k ? dbase : cbase;
         v[u] = __ldg(reinterpret_cast<const uint4 *>(b0 + static_cast<uint64_t>(m) * t));
       }
@@ -558,6 +570,8 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
       }
     }
   }
+  // a grid that read no check must still not complete before the precode grid (stream order)
+  if (!checks_ready) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ====================================================================== decoder (NEXT-1)
@@ -727,6 +741,15 @@ fs_status upload_graph(Graph &g) {
   return FS_OK;
 }
 
+// Programmatic dependent launch between dependent kernels of one call (FSB_PDL=0 disables).
+static bool pdl_enabled() {
+  static const int v = [] {
+    const char *e = std::getenv("FSB_PDL");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_t data_stride, uint8_t *checks,
                         uint64_t checks_stride, uint8_t *coded, uint64_t coded_stride, uint32_t row_begin,
                         uint32_t row_end, uint64_t col_begin, uint64_t col_end, void *stream_ptr, uint32_t *launches) {
@@ -837,10 +860,19 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     const uint32_t c0 = g.pre_level_ptr[L], nc = g.pre_level_ptr[L + 1] - c0;
     const uint64_t items = static_cast<uint64_t>(S) * nc * gslices;
     const uint64_t blocks = (items + kGroupsPerBlock - 1) / kGroupsPerBlock;
-    fsb_precode_global<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, c0, nc, prm.k, prm.d_p, prm.t, col_begin, col_end, gslices, g.dev.pre_col, data, data_stride, checks,
-        checks_stride);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_precode_global launch");
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(static_cast<uint32_t>(blocks));
+    lc.blockDim = dim3(kGlobalThreads);
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = pdl_enabled() && L > 0 ? 1 : 0;  // level L reads the checks of level L-1
+    e = cudaLaunchKernelEx(&lc, fsb_precode_global, S, c0, nc, prm.k, prm.d_p, prm.t, col_begin, col_end, gslices,
+                           static_cast<const int32_t *>(g.dev.pre_col), data, data_stride, checks, checks_stride);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "fsb_precode_global launch");
     ++*launches;
   }
   const uint32_t nrows = row_end - row_begin;
@@ -868,11 +900,22 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     auto kern = fsb_lt_band<2, 8>;
     if (band_cfg == 0) kern = fsb_lt_band<4, 6>;
     if (band_cfg == 2) kern = fsb_lt_band<8, 4>;
-    kern<<<static_cast<uint32_t>(blocks), kGlobalThreads, 0, stream>>>(
-        S, prm.k, static_cast<uint32_t>(prm.t), static_cast<uint32_t>(col_begin), static_cast<uint32_t>(col_end),
-        nbands, row_begin, nrows, band_rows, g.dev.lt_row_ptr,
-        g.dev.lt_colf, data, data_stride, checks, checks_stride, coded, coded_stride);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_lt_band launch");
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(static_cast<uint32_t>(blocks));
+    lc.blockDim = dim3(kGlobalThreads);
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = pdl_enabled() && prm.p ? 1 : 0;  // overlaps the precode launch
+    e = cudaLaunchKernelEx(&lc, kern, S, prm.k, static_cast<uint32_t>(prm.t), static_cast<uint32_t>(col_begin),
+                           static_cast<uint32_t>(col_end), nbands, row_begin, nrows, band_rows,
+                           static_cast<const int32_t *>(g.dev.lt_row_ptr), static_cast<const uint32_t *>(g.dev.lt_colf),
+                           data, data_stride, static_cast<const uint8_t *>(checks), checks_stride, coded,
+                           coded_stride);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "fsb_lt_band launch");
     ++*launches;
   }
   return FS_OK;
@@ -1034,10 +1077,6 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
     const uint32_t nsrc = static_cast<uint32_t>(pl.src_ptr[row0 + nrows] - pl.src_ptr[row0]);
     const bool long_rows = dpg_cfg == 2 || (dpg_cfg == 0 && nsrc >= 6u * nrows);
     auto kern = long_rows ? fsb_dpg_level<8, 4> : fsb_dpg_level<2, 6>;
-    static const int use_pdl = [] {
-      const char *e = std::getenv("FSB_PDL");
-      return e ? std::atoi(e) : 1;
-    }();
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(static_cast<uint32_t>(blocks));
     lc.blockDim = dim3(kGlobalThreads);
@@ -1047,7 +1086,7 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = attr;
-    lc.numAttrs = use_pdl && L > 0 ? 1 : 0;
+    lc.numAttrs = pdl_enabled() && L > 0 ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&lc, kern, S, static_cast<uint32_t>(pl.t), nbands, row0, nrows, band_rows,
                                        static_cast<const int32_t *>(pl.d_target),
                                        static_cast<const int32_t *>(pl.d_src_ptr),
