@@ -226,6 +226,8 @@ def main():
                     help="single-stripe configs at N>1: split coded rows (source replicated, BASELINE "
                          "config 5) or byte columns (fs_encode_range, nothing replicated)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-chunks", type=int, default=16, help="e2e: stripe chunks per step")
+    ap.add_argument("--e2e-streams", type=int, default=2, help="e2e: copy/compute streams")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -568,22 +570,23 @@ def _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all):
     h_data.copy_(data.cpu())
     h_chk = torch.empty((S, p, t), dtype=torch.uint8, pin_memory=True) if p else None
     h_cod = torch.empty((S, n, t), dtype=torch.uint8, pin_memory=True)
-    nchunks = min(S, 16)
+    nchunks = min(S, args.e2e_chunks)
+    ns = args.e2e_streams
     bounds = [(i * S // nchunks, (i + 1) * S // nchunks) for i in range(nchunks)]
-    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(ns)]
     cs = max(b - a for a, b in bounds)
-    d_buf = [torch.empty((cs, k, t), dtype=torch.uint8, device=dev) for _ in range(2)]
-    c_buf = [torch.empty((cs, p, t), dtype=torch.uint8, device=dev) if p else None for _ in range(2)]
-    y_buf = [torch.empty((cs, n, t), dtype=torch.uint8, device=dev) for _ in range(2)]
+    d_buf = [torch.empty((cs, k, t), dtype=torch.uint8, device=dev) for _ in range(ns)]
+    c_buf = [torch.empty((cs, p, t), dtype=torch.uint8, device=dev) if p else None for _ in range(ns)]
+    y_buf = [torch.empty((cs, n, t), dtype=torch.uint8, device=dev) for _ in range(ns)]
 
     def one_step():
         for i, (a, b) in enumerate(bounds):
-            st = streams[i % 2]
+            st = streams[i % ns]
             with torch.cuda.stream(st):
-                db = d_buf[i % 2][:b - a]
+                db = d_buf[i % ns][:b - a]
                 db.copy_(h_data[a:b], non_blocking=True)
-                cb = c_buf[i % 2][:b - a] if p else None
-                yb = y_buf[i % 2][:b - a]
+                cb = c_buf[i % ns][:b - a] if p else None
+                yb = y_buf[i % ns][:b - a]
                 g.encode_stripes(db, cb, yb, stream=st)
                 if p:
                     h_chk[a:b].copy_(cb, non_blocking=True)
@@ -612,7 +615,7 @@ def _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all):
     return {"value": round(src_bytes_all / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": S * k * t, "d2h_bytes_per_step": S * (p + n) * t,
             "ms_per_step": round(ms, 3),
-            "api": "fs_encode_stripes on pinned-host staging, %d chunks x 2 streams" % nchunks, "checked": ok}
+            "api": "fs_encode_stripes on pinned-host staging, %d chunks x %d streams" % (nchunks, ns), "checked": ok}
 
 
 if __name__ == "__main__":
