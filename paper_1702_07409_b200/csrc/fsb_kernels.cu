@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
     fsb_dpg_level(uint32_t S, uint32_t t, uint32_t nbands, uint32_t row0, uint32_t nrows, uint32_t band_rows,
                   const int32_t *__restrict__ target, const int32_t *__restrict__ src_ptr,
                   const uint32_t *__restrict__ src, uint8_t *coded, uint64_t coded_stride,
-                  uint8_t *inter, uint64_t inter_stride, uint8_t *work, uint64_t work_stride) {
+                  uint8_t *inter, uint64_t inter_stride, uint8_t *work, uint64_t work_stride, uint32_t rev) {
   // programmatic dependent launch: this level's CTAs may be scheduled while the previous level
   // drains; they wait here until it has completed and its writes are visible, and let the next
   // level be scheduled as soon as every CTA of this one has started
@@ -592,12 +592,16 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nchunks = (nrows + band_rows - 1) / band_rows;
+  const uint64_t total = static_cast<uint64_t>(S) * nbands * nchunks;
   uint64_t unit = static_cast<uint64_t>(blockIdx.x) * (kGlobalThreads / 32) + (threadIdx.x >> 5);
+  if (unit >= total) return;
+  // serpentine: odd levels sweep (stripe, band) backwards, so a level starts on the bands the
+  // previous one touched last (still in L2)
+  if (rev) unit = total - 1 - unit;
   const uint32_t chunk = static_cast<uint32_t>(unit % nchunks);
   unit /= nchunks;
   const uint32_t band = static_cast<uint32_t>(unit % nbands);
   const uint64_t s = unit / nbands;
-  if (s >= S) return;
   const uint32_t byte_raw = band * kBandBytes + lane * 16;
   const bool active = byte_raw < t;
   const uint32_t byte = active ? byte_raw : 0;
@@ -739,6 +743,15 @@ fs_status upload_graph(Graph &g) {
     }
   }
   return FS_OK;
+}
+
+// Odd plan levels sweep their (stripe, band) units backwards (FSB_SERPENTINE=0 disables).
+static bool serpentine() {
+  static const int v = [] {
+    const char *e = std::getenv("FSB_SERPENTINE");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
 }
 
 // Programmatic dependent launch between dependent kernels of one call (FSB_PDL=0 disables).
@@ -1091,7 +1104,7 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
                                        static_cast<const int32_t *>(pl.d_target),
                                        static_cast<const int32_t *>(pl.d_src_ptr),
                                        static_cast<const uint32_t *>(pl.d_src), coded, coded_stride, inter,
-                                       inter_stride, work, work_stride);
+                                       inter_stride, work, work_stride, serpentine() ? static_cast<uint32_t>(L & 1) : 0u);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "fsb_dpg_level launch");
     ++*launches;
