@@ -276,6 +276,18 @@ fs_status inactivation_phase(const Graph &g, const uint8_t *received, DecodePlan
     }
     if (express(D[x], zset)) final_row(x, true);
   }
+  // nothing beyond peeling is determined (e.g. the unrecovered symbols lie in no received
+  // equation's span): keep the peeling-only plan, no partial rows, no workspace
+  bool gained = false;
+  for (uint32_t m = 0; m < K && !gained; ++m) gained = pl.state[m] == 2;
+  if (!gained) {
+    for (uint32_t m = 0; m < K; ++m)
+      if (!pl.state[m]) pl.level_of[m] = -1;
+    pl.eliminated = 0;
+    pl.inactivated = static_cast<uint32_t>(inact.size());
+    pl.work_rows = 0;
+    return FS_OK;
+  }
   // emit the rows level by level after the DPG levels (stable within a level)
   int32_t any_recv = -1;
   for (uint32_t j = 0; j < n && any_recv < 0; ++j)
