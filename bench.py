@@ -475,7 +475,31 @@ def run_decode(args, cfg):
                         "algorithmic_bytes_per_step": b_hbm, "peak_source": peak_src,
                         "kernel": "fsb_dpg_level x %d launches" % launches},
            "gpu_launches": launches * args.steps, "checked": ok, "clocks": clk}
+    if not args.no_cpu:
+        out["cpu_baseline"] = _oracle_decode_sample(cfg, recv, cod, args)
     print(json.dumps(out))
+
+
+def _oracle_decode_sample(cfg, recv, cod, args):
+    """The oracle's decoder (Alg 1 BP over LT rows + precode checks, then GF(2) elimination when
+    --eliminate), single-threaded C, on whole stripes until ~--cpu-seconds (at least one); metric
+    = recovered data bytes per second, as the GPU line's."""
+    import numpy as np
+    import oracle
+    go = oracle.generate_graph(cfg)
+    S, k, t = cfg["stripes"], cfg["k"], cfg["t"]
+    done, t_dec, rec_bytes = 0, 0.0, 0
+    while done < S and (t_dec < args.cpu_seconds or done == 0):
+        Y = cod[done].cpu().numpy()
+        t0 = time.perf_counter()
+        _, state = oracle.decode(go, recv, Y, use_elim=bool(args.eliminate))
+        t_dec += time.perf_counter() - t0
+        rec_bytes += int(np.count_nonzero(state[:k])) * t
+        done += 1
+    host = _host_cpu()
+    return {"value": rec_bytes / t_dec / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "host_cpu": host["model"], "sample": "%d of %d stripes, single-threaded C oracle decoder%s, %.2f s"
+            % (done, S, " + elimination" if args.eliminate else "", t_dec)}
 
 
 def run_repair(args, cfg):
