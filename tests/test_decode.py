@@ -190,3 +190,26 @@ def test_gpu_decode_eliminate_matches_oracle(cid, frac, S):
         assert np.array_equal(st != 0, rec)
         assert np.array_equal(I[s][rec], oI[rec])           # (unrecovered rows may hold partials)
         assert np.array_equal(I[s][:c["k"]][rec[:c["k"]]], D[s][rec[:c["k"]]])
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_plan_elimination_random_graphs(seed):
+    """Random small codes and reception patterns (incl. p = 0, all / none received): the
+    inactivation-completed plan = the oracle's BP + Gauss-Jordan state."""
+    rng = np.random.default_rng(500 + seed)
+    k = int(rng.integers(1, 80))
+    p = int(rng.integers(0, 8))
+    n = int(rng.integers(1, 160))
+    c = dict(name="r", k=k, p=p, d_p=int(rng.integers(1, min(k, 4) + 1)) if p else 0, n=n, t=16, stripes=1,
+             dist=configs.FINITE, seed=int(rng.integers(1, 1 << 40)),
+             fin_deg=configs.OMEGA_DEGREES, fin_prob=configs.OMEGA_PROBS)
+    go = oracle.generate_graph(c)
+    g = fsb.Graph.create(c, host_only=True)
+    D = inputs.stripe_data(c).numpy()[0]
+    _, Y = oracle.encode(go, D)
+    for frac in (0.0, 0.5, 0.8, 1.0):
+        recv = rng.random(n) < frac
+        _, ostate = oracle.decode(go, recv, Y, use_elim=True)
+        st, lev = fsb.DecodePlan(g, recv, host_only=True, eliminate=True).state()
+        assert np.array_equal(st, ostate), (seed, frac)
+        assert np.all((lev >= 0) == (st != 0))
