@@ -213,3 +213,36 @@ def test_plan_elimination_random_graphs(seed):
         st, lev = fsb.DecodePlan(g, recv, host_only=True, eliminate=True).state()
         assert np.array_equal(st, ostate), (seed, frac)
         assert np.all((lev >= 0) == (st != 0))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(6))
+def test_gpu_decode_eliminate_random_graphs(seed):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rng = np.random.default_rng(900 + seed)
+    k = int(rng.integers(8, 300))
+    p = int(rng.integers(0, 12))
+    n = int(k + p + rng.integers(0, 80))
+    c = dict(name="r", k=k, p=p, d_p=int(rng.integers(1, min(k, 4) + 1)) if p else 0, n=n,
+             t=int(rng.choice([16, 512, 1040])), stripes=2, dist=configs.RSD, rsd_c=0.1, rsd_delta=0.5,
+             seed=int(rng.integers(1, 1 << 40)))
+    try:
+        go = oracle.generate_graph(c)
+    except ValueError:
+        pytest.skip("RSD parameters rejected")
+    D = inputs.stripe_data(c).numpy()
+    _, Y = oracle.encode(go, D)
+    recv = rng.random(n) < float(rng.uniform(0.8, 1.0))
+    g = fsb.Graph.create(c)
+    plan = fsb.DecodePlan(g, recv, eliminate=True)
+    Yd = torch.from_numpy(Y).cuda()
+    Yd[:, ~torch.from_numpy(recv)] = 0x77
+    inter = torch.full((2, g.K, c["t"]), 0xA5, dtype=torch.uint8, device="cuda")
+    plan.decode(Yd, inter)
+    torch.cuda.synchronize()
+    I = inter.cpu().numpy()
+    for s in range(2):
+        oI, ostate = oracle.decode(go, recv, Y[s], use_elim=True)
+        rec = ostate != 0
+        assert np.array_equal(I[s][rec], oI[rec])
