@@ -198,13 +198,18 @@ def run_reference(args, cfg):
     per_step = args.ref_seconds / max(1, steps)
     for _ in range(warm):
         cpu_oracle_sample(cfg, 0.0, max_stripes=1)
-    vals = [cpu_oracle_sample(cfg, per_step) for _ in range(steps)]
+    vals, secs = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        vals.append(cpu_oracle_sample(cfg, per_step))
+        secs.append(time.perf_counter() - t0)
     v = statistics.median(x["value"] for x in vals)
     cb = dict(vals[0])
     cb["value"] = v
     cb["sample"] = "per step: " + vals[0]["sample"]
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
-           "steps": steps, "warmup": warm, "higher_is_better": True, "scaling": args.scaling,
+           "steps": steps, "warmup": warm, "ms_per_step": round(1e3 * statistics.median(secs), 3),
+           "higher_is_better": True, "scaling": args.scaling,
            "vs_baseline": None, "dtype": "u8", "data": DATA,
            "config": {"workload": cfg["name"], "k": cfg["k"], "p": cfg["p"], "n": cfg["n"],
                       "t": cfg["t"], "stripes": cfg["stripes"]},
