@@ -788,6 +788,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
   if (g.variant == FS_VARIANT_SMEM) {
     if (!g.smem_eligible) { set_error("SMEM variant not eligible for this graph"); return FS_EUNSUPPORTED; }
     use_smem = full_rows;  // row ranges always take the GLOBAL path
+    if (use_smem && tiles >= (1ull << 31)) { set_error("launch too large for the SMEM variant"); return FS_EINVAL; }
   } else if (g.variant == FS_VARIANT_AUTO) {
     use_smem = g.smem_eligible && full_rows && tiles >= 2ull * g.sm_count && tiles < (1ull << 31);
   }
