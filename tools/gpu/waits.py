@@ -18,6 +18,6 @@ for _ in range(10):
     g.encode_stripes(d, chk, cod)
 torch.cuda.synchronize()
 c = fsb.debug_counters()
-W = 20
+W = 24
 rows = [{"warp": w, "wait_frac": round(c[2 * w] / max(1, c[2 * w + 1]), 4)} for w in range(W)]
 print(json.dumps({"per_warp": rows, "mean_wait_frac": round(sum(r["wait_frac"] for r in rows) / W, 4)}))
