@@ -20,8 +20,8 @@ constexpr int kConsumerWarps = 24;
 constexpr int kHalvesPerWarp = 8;                        // half-groups: 4 lanes x 16 B = 64 B
 constexpr int kPrecodeWarps = 3;                         // precode (a3) warps per CTA
 constexpr int kThreads = (kConsumerWarps + 1 + kPrecodeWarps) * 32;  // + 1 TMA warp
-constexpr int kSplitThreshold = 48;                      // rows of degree > this are split:
-constexpr int kSplit2Max = 96;                           //   over the 2 halves of a group (<= this)
+constexpr int kSplitThreshold = 60;                      // rows of degree > this are split:
+constexpr int kSplit2Max = 120;                           //   over the 2 halves of a group (<= this)
                                                          //   or over the 8 half-groups of a warp
 
 // Bank rule: a 128-bit shared load is served in phases of 8 lanes = two half-groups (lanes
