@@ -106,8 +106,8 @@ typedef struct fs_graph fs_graph;  /* opaque */
                                    fs_encode* then return FS_EUNSUPPORTED.               */
 
 /* Kernel variants (fs_graph_set_variant).  All produce identical bytes. */
-#define FS_VARIANT_AUTO 0       /* per call: SMEM when eligible and the call has >= 2 tiles
-                                   per SM, else GLOBAL                                   */
+#define FS_VARIANT_AUTO 0       /* per call: SMEM when the graph is eligible and the call
+                                   covers all rows on 64-B slice boundaries, else GLOBAL */
 #define FS_VARIANT_SMEM 1       /* persistent TMA-staged shared-memory tile kernel        */
 #define FS_VARIANT_GLOBAL 2     /* L2-resident band sweep (precode kernel + LT kernel)    */
 

@@ -790,7 +790,10 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     use_smem = full_rows;  // row ranges always take the GLOBAL path
     if (use_smem && tiles >= (1ull << 31)) { set_error("launch too large for the SMEM variant"); return FS_EINVAL; }
   } else if (g.variant == FS_VARIANT_AUTO) {
-    use_smem = g.smem_eligible && full_rows && tiles >= 2ull * g.sm_count && tiles < (1ull << 31);
+    // SMEM whenever it can run the call: even a few tiles beat the band sweep, whose heavy rows
+    // are serial chains of L2 round trips (tools/gpu/auto_probe.py: configs 2/4/6/7 with 1-8
+    // stripes, 19-30 us vs 48-160 us; a tie only at config 1's 8 tiles)
+    use_smem = g.smem_eligible && full_rows && tiles < (1ull << 31);
   }
   if (S == 0 || row_end == row_begin) {
     if (S == 0 || prm.p == 0) return FS_OK;
