@@ -430,7 +430,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint4 h0 = lds128(hp);
     long long t_wait0 = 0;
     if (a.debug & 2) t_wait0 = clock64();
-    mbar_wait_backoff(smem_u32(&ready[b]), ph, a.wait_ns);
+    if (a.wait_ns) mbar_wait_backoff(smem_u32(&ready[b]), ph, a.wait_ns);
+    else mbar_wait(smem_u32(&ready[b]), ph);  // FSB_WAIT_NS=0: hardware-suspended try_wait
     mbar_wait(smem_u32(&full[b]), ph);
     if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2], static_cast<unsigned long long>(clock64() - t_wait0));
     // unpaired: this slice's 64 B; paired: the pair's 128-B line (slice s = the even one)
