@@ -513,6 +513,11 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
                 uint32_t nrows, uint32_t band_rows, const int32_t *__restrict__ row_ptr, const uint32_t *__restrict__ colf,
                 const uint8_t *__restrict__ data, uint64_t data_stride, const uint8_t *__restrict__ checks,
                 uint64_t checks_stride, uint8_t *__restrict__ coded, uint64_t coded_stride) {
+  // launched programmatically after the precode kernel (PDL): the CTAs are scheduled while it
+  // drains and wait here for its checks.  (Waiting only before a warp's first check source would
+  // overlap more, but a __ldg is an invariant load to the compiler and may be hoisted above the
+  // wait -- measured: with the wait deferred, a 4-deep batch read checks before they existed.)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nchunks = (nrows + band_rows - 1) / band_rows;
   uint64_t unit = static_cast<uint64_t>(blockIdx.x) * (kGlobalThreads / 32) + (threadIdx.x >> 5);
@@ -520,10 +525,7 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   unit /= nchunks;
   const uint32_t band = static_cast<uint32_t>(unit % nbands);
   const uint64_t s = unit / nbands;
-  if (s >= S) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // never complete before the precode grid
-    return;
-  }
+  if (s >= S) return;
   const uint32_t byte_raw = col0 + band * kBandBytes + lane * 16;  // bands cover columns [col0, col1)
   const bool active = byte_raw < col1;                // ragged last band
   const uint32_t byte = active ? byte_raw : col0;     // inactive lanes load a valid address
@@ -536,9 +538,6 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   const int32_t end = __ldg(&row_ptr[row_begin + r0 + rows]);
   uint8_t *out = coded + s * coded_stride + static_cast<uint64_t>(r0) * t + byte_raw;
   uint4 acc = make_uint4(0, 0, 0, 0);
-  // launched programmatically after the precode kernel (PDL): rows run while the checks are
-  // still being computed; a warp waits for the precode grid only before its first check source
-  bool checks_ready = false;
   for (int32_t e0 = base; e0 < end; e0 += 32) {
     // 32 marked column indices (bit 31 = last edge of its row) per coalesced load; positions
     // past `end` read row 0 and are never XORed
@@ -551,10 +550,6 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
       for (uint32_t u = 0; u < kBandBatch; ++u) {
         mr[u] = __shfl_sync(0xffffffffu, cv, kk + u);
         const uint32_t m = mr[u] & 0x7FFFFFFFu;
-        if (m >= k && !checks_ready) {  // warp-uniform: the precode launch must have completed
-          asm volatile("griddepcontrol.wait;" ::: "memory");
-          checks_ready = true;
-        }
         const uint8_t *b0 = m < k ? dbase : cbase;
         v[u] = __ldg(reinterpret_cast<const uint4 *>(b0 + static_cast<uint64_t>(m) * t));
       }
@@ -571,8 +566,6 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
       }
     }
   }
-  // a grid that read no check must still not complete before the precode grid (stream order)
-  if (!checks_ready) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ====================================================================== decoder (NEXT-1)
@@ -915,8 +908,10 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
       const char *e = std::getenv("FSB_BAND_CFG");
       return e ? std::atoi(e) : 4;
     }();
-    auto kern = fsb_lt_band<2, 8>;
-    if (band_cfg == 0) kern = fsb_lt_band<4, 6>;
+    // A call of only a few waves of warps ends on its heaviest rows' serial gather chains; there 4
+    // gathers in flight beat 2 (config 3: 35.2 -> 30.1 us; config 5, 13 waves, keeps (2, 8)).
+    const bool few_waves = units < 4ull * g.sm_count * 64;
+    auto kern = (band_cfg == 0 || (band_cfg == 4 && few_waves)) ? fsb_lt_band<4, 6> : fsb_lt_band<2, 8>;
     if (band_cfg == 2) kern = fsb_lt_band<8, 4>;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(static_cast<uint32_t>(blocks));
