@@ -624,7 +624,11 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
         fl[u] = __shfl_sync(0xffffffffu, cv, kk + u);
         const uint32_t m = fl[u] & kSrcIndex;
         const uint8_t *b0 = (fl[u] & kSrcCoded) ? cbase : (fl[u] & kSrcWork) ? wbase : ibase;
-        v[u] = __ldg(reinterpret_cast<const uint4 *>(b0 + static_cast<uint64_t>(m) * t));
+        // an asm volatile load: rows of earlier levels are written by the previous grid; an
+        // invariant __ldg could be hoisted above the griddepcontrol.wait at kernel entry
+        asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(b0 + static_cast<uint64_t>(m) * t));
       }
       const int32_t lim = min(static_cast<int32_t>(kBatch), nb - kk);
 #pragma unroll
