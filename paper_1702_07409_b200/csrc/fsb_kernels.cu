@@ -551,7 +551,9 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
         mr[u] = __shfl_sync(0xffffffffu, cv, kk + u);
         const uint32_t m = mr[u] & 0x7FFFFFFFu;
         const uint8_t *b0 = m < k ? dbase : cbase;
-        v[u] = __ldg(reinterpret_cast<const uint4 *>(b0 + static_cast<uint64_t>(m) * t));
+        asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(b0 + static_cast<uint64_t>(m) * t));
       }
       const int32_t lim = min(static_cast<int32_t>(kBandBatch), nb - kk);
 #pragma unroll
