@@ -280,7 +280,11 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+        t_bc = time.perf_counter()
         g = fdist.broadcast_graph(cfg, device=dev)        # step a2 over NCCL
+        torch.cuda.synchronize()
+        bcast_ms = fdist.max_over_ranks(1e3 * (time.perf_counter() - t_bc), device=dev)
     else:
         g = fsb.Graph.create(cfg)
     if args.variant != "auto":
@@ -388,6 +392,17 @@ def main():
                        "frac": round(b_gather / (launch_ms * 1e-3) / 1e9 / SMEM_GATHER_PEAK_GBS, 4),
                        "peak_source": "measured parity-paired 64-B smem row gather, tools/microbench/mb3.cu"}}
 
+    collectives = None
+    if ws > 1:
+        collectives = {"graph_broadcast_ms": round(bcast_ms, 3),
+                       "graph_broadcast": "rank 0 generates, NCCL broadcast of the CSR, every rank "
+                                          "rebuilds its schedule; host wall clock, max over ranks"}
+        if kind == "stripes" and args.scaling == "strong":
+            try:
+                collectives["result_gather"] = _time_gather(cod, cfg["stripes"], dev, ws)
+            except Exception as e:  # reported, never fatal to the encode line
+                collectives["result_gather"] = {"error": repr(e)[:300]}
+
     e2e = None
     if args.e2e_steps > 0 and kind == "stripes":
         e2e = _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all)
@@ -412,7 +427,10 @@ def main():
                              % (work_bytes / 1e9)),
                       "lt_nnz": inf["lt_nnz"], "max_degree": inf["max_degree"]},
            "roofline": roof, "gpu_launches": launches_per_step * args.steps,
-           "step_ms_median": round(statistics.median(per), 5), "clocks": clk, "e2e": e2e}
+           "step_ms_median": round(statistics.median(per), 5), "step_ms_best": round(min(per), 5),
+           "clocks": clk, "e2e": e2e}
+    if collectives:
+        out["collectives"] = collectives
     if args.graph_replay and ws == 1:
         out["graph_replay"] = _graph_replay(step, stream, args.graph_replay, src_bytes_all)
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -592,6 +610,30 @@ def run_repair(args, cfg):
                         "kernel": "fsb_dpg_level x %d launches" % launches},
            "gpu_launches": launches * args.steps, "checked": ok, "clocks": clk}
     print(json.dumps(out))
+
+
+def _time_gather(cod, total, dev, ws, reps=3):
+    """SURVEY.md §8(e)(ii), reported apart from the encode: every rank's coded stripes to rank 0
+    (dist.gather_stripes, NCCL point-to-point).  CUDA events per rep, max over ranks."""
+    import torch.distributed as dist
+    dist.barrier()
+    fdist.gather_stripes(cod, total)                     # warm-up (NCCL P2P setup)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(reps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fdist.gather_stripes(cod, total)
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(fdist.max_over_ranks(a.elapsed_time(b), device=dev))
+        del out
+    moved = (total - fdist.shard(total, ws, 0)[1]) * cod[0].numel()
+    best = min(ms)
+    return {"ms": round(best, 3), "bytes_to_rank0": moved, "GBps_into_rank0": round(moved / (best * 1e-3) / 1e9, 1),
+            "reps": reps, "timing": "CUDA events on the current stream, best of reps, max over ranks"}
 
 
 def _graph_replay(step, stream, count, src_bytes):

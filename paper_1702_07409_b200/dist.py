@@ -61,6 +61,32 @@ def broadcast_graph(cfg, group=None, device="cpu", host_only=False):
     return fsb.Graph.from_csr(cfg, *parts, host_only=host_only)
 
 
+def gather_stripes(local, total, group=None):
+    """the coded output to rank 0.  Every rank holds its contiguous stripe
+    shard (`shard(total, world_size, rank)`) as `local` [S_r, ...]; rank 0 returns the whole
+    [total, ...] tensor, the other ranks None.  Point-to-point receives straight into rank 0's
+    slices (shards may differ in size by one, so no equal-size gather)."""
+    import torch.distributed as dist
+    ws, rank = dist.get_world_size(group), dist.get_rank(group)
+    if rank != 0:
+        if local.shape[0]:
+            for req in dist.batch_isend_irecv([dist.P2POp(dist.isend, local.contiguous(), 0, group)]):
+                req.wait()
+        return None
+    out = torch.empty((total,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    b0, e0 = shard(total, ws, 0)
+    out[b0:e0].copy_(local)
+    ops = []
+    for r in range(1, ws):
+        b, e = shard(total, ws, r)
+        if e > b:
+            ops.append(dist.P2POp(dist.irecv, out[b:e], r, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return out
+
+
 def max_over_ranks(value, group=None, device="cpu"):
     """The max of a float over all ranks (the bench's timing rule)."""
     import torch.distributed as dist

@@ -114,3 +114,42 @@ def test_bench_plan_cols():
         parts = [bench.plan(c5, ws, r, "strong", "cols") for r in range(ws)]
         assert all(k == "cols" for k, _, _ in parts)
         assert parts[0][1] == 0 and parts[-1][2] == c5["t"]
+
+
+def _gather_worker(rank, ws, port, total, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=ws)
+        b, e = fdist.shard(total, ws, rank)
+        # stripe s of the job = bytes (s * 7 + column) & 0xFF: rank 0 can check every slice
+        local = ((torch.arange(b, e).view(-1, 1, 1) * 7 + torch.arange(96).view(1, 1, -1)) & 0xFF)
+        local = local.expand(e - b, 3, 96).to(torch.uint8).contiguous()
+        out = fdist.gather_stripes(local, total)
+        ok = None
+        if rank == 0:
+            want = ((torch.arange(total).view(-1, 1, 1) * 7 + torch.arange(96).view(1, 1, -1)) & 0xFF)
+            ok = bool(torch.equal(out, want.expand(total, 3, 96).to(torch.uint8)))
+        else:
+            ok = out is None
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, ok))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("ws,total", [(2, 5), (3, 7), (3, 2)])
+def test_gather_stripes_to_rank0(ws, total):
+    """§8(e)(ii): every rank's contiguous stripe shard lands in its slice of rank 0's output
+    (ragged shards, and a rank with no stripes)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, ws, port, total, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok is True for _, ok in res), res
