@@ -649,6 +649,80 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   }
 }
 
+// Levels of long rows (late decode levels, repair / update rows: tens to hundreds of sources):
+// in fsb_dpg_level a warp walks a row's sources one 512-B gather after another, a serial chain
+// of L2 / HBM round trips.  Here a warp covers a 128-B band of its rows as four 8-lane groups:
+// group g gathers sources g, g+4, g+8, ... of the row (each group load is one full 128-B line),
+// so one load instruction fetches four different sources, and the groups' partial XORs are
+// combined by two shuffles.  Units are (stripe, 128-B band, chunk of rows), rows one at a time.
+constexpr uint32_t kQBandBytes = 128;
+template <uint32_t kBatch, int kMinBlocks>
+__global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
+    fsb_dpg_level_q(uint32_t S, uint32_t t, uint32_t nbands, uint32_t row0, uint32_t nrows, uint32_t band_rows,
+                    const int32_t *__restrict__ target, const int32_t *__restrict__ src_ptr,
+                    const uint32_t *__restrict__ src, uint8_t *coded, uint64_t coded_stride, uint8_t *inter,
+                    uint64_t inter_stride, uint8_t *work, uint64_t work_stride, uint32_t rev) {
+  static_assert(kBatch == 1 || kBatch == 2 || kBatch == 4 || kBatch == 8, "4 groups x kBatch must divide 32");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t lane = threadIdx.x & 31, grp = lane >> 3;
+  const uint32_t nchunks = (nrows + band_rows - 1) / band_rows;
+  const uint64_t total = static_cast<uint64_t>(S) * nbands * nchunks;
+  uint64_t unit = static_cast<uint64_t>(blockIdx.x) * (kGlobalThreads / 32) + (threadIdx.x >> 5);
+  if (unit >= total) return;
+  if (rev) unit = total - 1 - unit;
+  const uint32_t chunk = static_cast<uint32_t>(unit % nchunks);
+  unit /= nchunks;
+  const uint32_t band = static_cast<uint32_t>(unit % nbands);
+  const uint64_t s = unit / nbands;
+  const uint32_t byte_raw = band * kQBandBytes + (lane & 7) * 16;
+  const bool active = byte_raw < t;
+  const uint32_t byte = active ? byte_raw : 0;
+  const uint8_t *ibase = inter + s * inter_stride + byte;
+  const uint8_t *cbase = coded + s * coded_stride + byte;
+  const uint8_t *wbase = work + s * work_stride + byte;
+  const uint32_t r0 = row0 + chunk * band_rows;
+  const uint32_t rows = min(band_rows, row0 + nrows - r0);
+  for (uint32_t r = r0; r < r0 + rows; ++r) {
+    const int32_t a = __ldg(&src_ptr[r]), b = __ldg(&src_ptr[r + 1]);
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (int32_t e0 = a; e0 < b; e0 += 32) {
+      const uint32_t cv = e0 + static_cast<int32_t>(lane) < b ? __ldg(&src[e0 + lane]) : kSrcCoded;
+      const int32_t nb = min(32, b - e0);
+      for (int32_t kk = 0; kk < nb; kk += 4 * kBatch) {
+        uint4 v[kBatch];
+#pragma unroll
+        for (uint32_t u = 0; u < kBatch; ++u) {
+          const int32_t pos = kk + 4 * static_cast<int32_t>(u) + static_cast<int32_t>(grp);
+          const uint32_t f = __shfl_sync(0xffffffffu, cv, pos & 31);
+          const uint32_t m = f & kSrcIndex;
+          const uint8_t *b0 = (f & kSrcCoded) ? cbase : (f & kSrcWork) ? wbase : ibase;
+          v[u] = make_uint4(0, 0, 0, 0);
+          if (pos < nb)  // (group-uniform) past the row's end: nothing to gather
+            asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                         : "l"(b0 + static_cast<uint64_t>(m) * t));
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < kBatch; ++u) xor_into(acc, v[u]);
+      }
+    }
+#pragma unroll
+    for (int o = 8; o <= 16; o <<= 1) {
+      acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, o);
+      acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, o);
+      acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, o);
+    }
+    if (grp == 0 && active) {
+      const uint32_t f = static_cast<uint32_t>(__ldg(&target[r]));
+      uint8_t *ob = (f & kSrcCoded) ? coded + s * coded_stride : (f & kSrcWork) ? work + s * work_stride
+                                                                                : inter + s * inter_stride;
+      *reinterpret_cast<uint4 *>(ob + static_cast<uint64_t>(f & kSrcIndex) * t + byte_raw) = acc;
+    }
+  }
+}
+
 // ===================================================================== host-side launch
 namespace {
 
@@ -1071,6 +1145,11 @@ fs_status launch_plan(const DecodePlan &pl, uint32_t S, uint8_t *coded, uint64_t
   return FS_OK;
 }
 
+// rows per unit of a level: as many as keep >= 64 warps' worth of units per SM (1..8)
+static uint32_t level_band_rows(uint64_t row_bands, int sm_count) {
+  return static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kBandRowsMax, row_bands / (64ull * sm_count))));
+}
+
 static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded, uint64_t coded_stride,
                                uint8_t *inter, uint64_t inter_stride, uint8_t *work, uint64_t work_stride,
                                cudaStream_t stream, uint32_t *launches) {
@@ -1080,11 +1159,8 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
     const uint32_t row0 = pl.level_ptr[L], nrows = pl.level_ptr[L + 1] - row0;
     if (!nrows) continue;
     const uint64_t row_bands = static_cast<uint64_t>(S) * nbands * nrows;
-    const uint32_t band_rows = static_cast<uint32_t>(
-        std::max<uint64_t>(1, std::min<uint64_t>(kBandRowsMax, row_bands / (64ull * pl.sm_count))));
+    const uint32_t band_rows = level_band_rows(row_bands, pl.sm_count);
     const uint64_t units = static_cast<uint64_t>(S) * nbands * ((nrows + band_rows - 1) / band_rows);
-    const uint64_t blocks = (units + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
-    if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
     // gathers in flight per warp: levels of long rows (repair / update / dense decode levels) take 8
     // at 4 blocks per SM, levels of short rows 2 at 6 blocks (measured on configs 5, 7 and 4:
     // update 3.41 -> 3.10 ms, repair 0.457 -> 0.384, decode 0.722 -> 0.687 with 8 in flight; the
@@ -1096,6 +1172,37 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
     const uint32_t nsrc = static_cast<uint32_t>(pl.src_ptr[row0 + nrows] - pl.src_ptr[row0]);
     const bool long_rows = dpg_cfg == 2 || (dpg_cfg == 0 && nsrc >= 6u * nrows);
     auto kern = long_rows ? fsb_dpg_level<8, 4> : fsb_dpg_level<2, 6>;
+    // Levels of very long rows (>= FSB_DPG_Q sources on average; update: ~234) with enough units
+    // for >= 4 waves: four source streams per warp over 128-B bands (fsb_dpg_level_q<4, 6>).
+    // Measured (one box, tools/gpu/dpgq_sweep.sh): update 3.11 -> 2.34 ms; it loses where the
+    // rows are shorter (decode's late levels, 30-60 sources: 0.655 -> 0.664-0.72 ms) or the level
+    // is too small to fill the GPU (repair's 13 rows: 0.384 -> 0.42-0.53 ms).
+    static const uint32_t q_min = [] {
+      const char *e = std::getenv("FSB_DPG_Q");
+      return e ? static_cast<uint32_t>(std::atoi(e)) : 100u;
+    }();
+    static const int q_cfg = [] {
+      const char *e = std::getenv("FSB_DPG_QCFG");
+      return e ? std::atoi(e) : 1;
+    }();
+    static const int q_rows = [] {
+      const char *e = std::getenv("FSB_DPG_QROWS");
+      return e ? std::atoi(e) : 0;
+    }();
+    uint32_t nb = nbands, br = band_rows;
+    uint64_t nunits = units;
+    if (q_min && nsrc >= static_cast<uint64_t>(q_min) * nrows) {
+      const uint32_t qnb = static_cast<uint32_t>((pl.t + kQBandBytes - 1) / kQBandBytes);
+      const uint32_t qbr = q_rows > 0 ? std::min<uint32_t>(kBandRowsMax, static_cast<uint32_t>(q_rows))
+                                      : level_band_rows(static_cast<uint64_t>(S) * qnb * nrows, pl.sm_count);
+      const uint64_t qunits = static_cast<uint64_t>(S) * qnb * ((nrows + qbr - 1) / qbr);
+      if (q_min == 1 || qunits >= 4ull * pl.sm_count * 48) {  // FSB_DPG_Q=1: every level (tests)
+        kern = q_cfg == 0 ? fsb_dpg_level_q<8, 4> : q_cfg == 2 ? fsb_dpg_level_q<2, 8> : fsb_dpg_level_q<4, 6>;
+        nb = qnb, br = qbr, nunits = qunits;
+      }
+    }
+    const uint64_t blocks = (nunits + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
+    if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(static_cast<uint32_t>(blocks));
     lc.blockDim = dim3(kGlobalThreads);
@@ -1106,7 +1213,7 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = attr;
     lc.numAttrs = pdl_enabled() && L > 0 ? 1 : 0;
-    cudaError_t e = cudaLaunchKernelEx(&lc, kern, S, static_cast<uint32_t>(pl.t), nbands, row0, nrows, band_rows,
+    cudaError_t e = cudaLaunchKernelEx(&lc, kern, S, static_cast<uint32_t>(pl.t), nb, row0, nrows, br,
                                        static_cast<const int32_t *>(pl.d_target),
                                        static_cast<const int32_t *>(pl.d_src_ptr),
                                        static_cast<const uint32_t *>(pl.d_src), coded, coded_stride, inter,

@@ -323,3 +323,50 @@ def test_gpu_update_equals_encode():
     assert inf["repaired"] > 0
     ok = (cod[:, g.n:] == full[:, g.n:]).flatten(2).all(-1).cpu().numpy()    # [S, new rows]
     assert ok.sum(1).tolist() == [inf["repaired"]] * S
+
+
+@pytest.mark.gpu
+def test_gpu_update_long_rows_many_stripes():
+    """Update of config 7's code at 64 stripes: one level of 130 new rows of ~234 sources, enough
+    units for the long-row level kernel (fsb_dpg_level_q); the rebuilt rows equal fs_encode's."""
+    _need_gpu()
+    c = dict(configs.get(7), stripes=64)
+    g = fsb.Graph.create(c)
+    ch = fsb.Checks.create(g, 3)
+    g2 = g.extend(1)
+    ch2 = fsb.Checks.from_data(g2, ch.data())
+    S = c["stripes"]
+    d = inputs.stripe_data(c, device="cuda")
+    full = torch.empty((S, g2.n, g2.t), dtype=torch.uint8, device="cuda")
+    chk = torch.empty((S, g2.p, g2.t), dtype=torch.uint8, device="cuda")
+    g2.encode_stripes(d, chk, full)
+    mask = np.zeros(g2.n, bool)
+    mask[g.n:] = True
+    rp = fsb.RepairPlan(g2, ch2, mask)
+    inf = rp.info()
+    assert inf["xor_sources"] >= 100 * inf["rows"]
+    cod = full.clone()
+    cod[:, g.n:] = 0
+    rp.repair(cod)
+    torch.cuda.synchronize()
+    ok = (cod[:, g.n:] == full[:, g.n:]).flatten(2).all(-1).cpu().numpy()
+    assert ok.sum(1).tolist() == [inf["repaired"]] * S
+    assert inf["repaired"] == g2.n - g.n
+
+
+@pytest.mark.gpu
+def test_gpu_long_row_kernel_on_every_level():
+    """FSB_DPG_Q=1 routes every plan level through fsb_dpg_level_q (the knob is read once per
+    process, so in a child pytest): the decode and repair parity tests must still pass."""
+    _need_gpu()
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FSB_DPG_Q="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_decode.py::test_gpu_decode_matches_oracle",
+                        "tests/test_decode.py::test_gpu_decode_eliminate_matches_oracle",
+                        "tests/test_repair.py::test_gpu_repair_parity",
+                        "tests/test_repair.py::test_gpu_update_equals_encode"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
