@@ -506,6 +506,7 @@ __global__ void __launch_bounds__(kGlobalThreads)
 // source about once, the gathers hit L2.
 constexpr uint32_t kBandBytes = 512;
 constexpr uint32_t kBandRowsMax = 8;   // coded rows per warp (fewer when the call is small)
+constexpr uint32_t kQBandBytes = 128;  // band of the four-group long-row level kernel
 
 template <uint32_t kBandBatch, int kMinBlocks>
 __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
@@ -655,7 +656,6 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
 // group g gathers sources g, g+4, g+8, ... of the row (each group load is one full 128-B line),
 // so one load instruction fetches four different sources, and the groups' partial XORs are
 // combined by two shuffles.  Units are (stripe, 128-B band, chunk of rows), rows one at a time.
-constexpr uint32_t kQBandBytes = 128;
 template <uint32_t kBatch, int kMinBlocks>
 __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
     fsb_dpg_level_q(uint32_t S, uint32_t t, uint32_t nbands, uint32_t row0, uint32_t nrows, uint32_t band_rows,
