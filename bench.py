@@ -231,10 +231,14 @@ def main():
                     help="single-stripe configs at N>1: split coded rows (source replicated, BASELINE "
                          "config 5) or byte columns (fs_encode_range, nothing replicated)")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--e2e-chunks", type=int, default=16, help="e2e: stripe chunks per step")
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="e2e: chunks per step (0: the library's default for --e2e-api host, 16 for stripes)")
     ap.add_argument("--graph-replay", type=int, default=0,
                     help="also time N steps captured in one CUDA graph (small configs, warm L2)")
     ap.add_argument("--e2e-streams", type=int, default=2, help="e2e: copy/compute streams")
+    ap.add_argument("--e2e-api", choices=["host", "stripes"], default="host",
+                    help="e2e through fs_encode_host (library staging) or fs_encode_stripes on "
+                         "bench-managed staging")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -405,7 +409,10 @@ def main():
 
     e2e = None
     if args.e2e_steps > 0 and kind == "stripes":
-        e2e = _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all)
+        if args.e2e_api == "host":
+            e2e = _e2e_host(g, cfg, data, cod, S, args, dev, ws, src_bytes_all)
+        else:
+            e2e = _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all)
 
     out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
@@ -662,6 +669,38 @@ def _graph_replay(step, stream, count, src_bytes):
             "value": round(src_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "l2": "warm"}
 
 
+def _e2e_host(g, cfg, data, cod, S, args, dev, ws, src_bytes_all):
+    """The metric through fs_encode_host: every step hands the library the HOST buffers (pinned)
+    and it stages them through its own device memory -- H2D of the data, the encode, D2H of
+    checks + coded, pipelined over chunks of stripes (or of byte columns for one stripe)."""
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    h_data = torch.empty((S, k, t), dtype=torch.uint8, pin_memory=True)
+    h_data.copy_(data.cpu())
+    h_chk = torch.empty((S, p, t), dtype=torch.uint8, pin_memory=True) if p else None
+    h_cod = torch.empty((S, n, t), dtype=torch.uint8, pin_memory=True)
+    cur = torch.cuda.current_stream(dev)
+    g.encode_host(h_data, h_chk, h_cod, chunks=args.e2e_chunks, stream=cur)  # warm: staging allocated
+    torch.cuda.synchronize()
+    launches = fsb.last_launch_count()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cur)
+    for _ in range(args.e2e_steps):
+        g.encode_host(h_data, h_chk, h_cod, chunks=args.e2e_chunks, stream=cur)
+    e1.record(cur)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ms = (fdist.max_over_ranks(ms, device=dev) if ws > 1 else ms) / args.e2e_steps
+    ok = bool(torch.equal(h_cod[0].to(dev), cod[0]) and torch.equal(h_cod[S - 1].to(dev), cod[S - 1]))
+    return {"value": round(src_bytes_all / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": S * k * t, "d2h_bytes_per_step": S * (p + n) * t,
+            "ms_per_step": round(ms, 3), "gpu_launches_per_step": launches,
+            "api": "fs_encode_host (library staging, %s chunks of %s, 2 library streams)"
+                   % (args.e2e_chunks or "default", "stripes" if S > 1 else "byte columns"), "checked": ok}
+
+
 def _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all):
     """Same metric through fs_encode_stripes with HOST buffers: per step, H2D of the step's
     data from pinned memory, the encode, and D2H of checks + coded, pipelined over chunks of
@@ -671,7 +710,7 @@ def _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all):
     h_data.copy_(data.cpu())
     h_chk = torch.empty((S, p, t), dtype=torch.uint8, pin_memory=True) if p else None
     h_cod = torch.empty((S, n, t), dtype=torch.uint8, pin_memory=True)
-    nchunks = min(S, args.e2e_chunks)
+    nchunks = min(S, args.e2e_chunks or 16)
     ns = args.e2e_streams
     bounds = [(i * S // nchunks, (i + 1) * S // nchunks) for i in range(nchunks)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(ns)]

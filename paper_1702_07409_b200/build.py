@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfsb200.so")
-SOURCES = ["fsb_kernels.cu", "fsb_graph.cpp", "fsb_decode.cpp", "fsb_repair.cpp", "fsb_capi.cpp"]
+SOURCES = ["fsb_kernels.cu", "fsb_graph.cpp", "fsb_decode.cpp", "fsb_repair.cpp", "fsb_io.cpp", "fsb_capi.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2,-ffp-contract=off,-fvisibility=hidden", "-Xptxas", "-v",

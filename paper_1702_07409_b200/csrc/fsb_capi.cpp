@@ -235,6 +235,48 @@ fs_status fs_encode_stripes(const fs_graph *h, uint32_t S, const uint8_t *d_data
   return st;
 }
 
+fs_status fs_encode_host(const fs_graph *h, uint32_t S, const uint8_t *h_data, uint64_t data_stride,
+                         uint8_t *h_checks, uint64_t checks_stride, uint8_t *h_coded, uint64_t coded_stride,
+                         uint32_t chunks, void *stream) {
+  fsb::set_error("");
+  fsb::g_launches = 0;
+  fs_status st = check_device_graph(h);
+  if (st != FS_OK) return st;
+  const fsb::Graph &g = h->g;
+  if (S == 0) return FS_OK;
+  const uint64_t t = g.prm.t, k = g.prm.k, p = g.prm.p, n = g.prm.n;
+  if (S == 1) {  // one stripe: symbols contiguous (the column chunks are strided by t)
+    data_stride = std::max(data_stride, k * t);
+    checks_stride = std::max(checks_stride, p * t);
+    coded_stride = std::max(coded_stride, n * t);
+  }
+  if (!h_data || data_stride < k * t) { set_error("h_data must be non-NULL with data_stride >= k*t"); return FS_EINVAL; }
+  if (p > 0 && (!h_checks || checks_stride < p * t)) {
+    set_error("h_checks must be non-NULL with checks_stride >= p*t when p > 0");
+    return FS_EINVAL;
+  }
+  if (p == 0 && h_checks) { set_error("h_checks must be NULL when p == 0"); return FS_EINVAL; }
+  if (!h_coded || coded_stride < n * t) { set_error("h_coded must be non-NULL with coded_stride >= n*t"); return FS_EINVAL; }
+  {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != g.dev.device) {
+      set_error("the graph lives on device " + std::to_string(g.dev.device) + ", the current device is " +
+                std::to_string(cur));
+      return FS_EINVAL;
+    }
+  }
+  fs_graph *hm = const_cast<fs_graph *>(h);  // the staging cache is the graph's, not its contents
+  std::lock_guard<std::mutex> lock(hm->io_mu);
+  if (!hm->io) hm->io.reset(new (std::nothrow) fsb::IoCache());
+  if (!hm->io) { set_error("out of host memory"); return FS_ENOMEM; }
+  uint32_t launches = 0;
+  st = fsb::encode_host(g, *hm->io, S, h_data, data_stride, h_checks, checks_stride, h_coded, coded_stride,
+                        chunks ? chunks : 32u, stream, &launches);
+  if (st == FS_OK) fsb::g_launches = launches;
+  return st;
+}
+
 fs_status fs_graph_schedule(const fs_graph *h, const uint32_t **words, uint64_t *nwords, uint32_t *cont_base,
                             const uint32_t **warp_info, uint32_t *nwarps, uint32_t *kpad, uint32_t *zero_even) {
   if (!h) { set_error("null graph"); return FS_EINVAL; }

@@ -1,7 +1,10 @@
 // Internal declarations of libfsb200 (not part of the C ABI).
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -122,8 +125,25 @@ void set_error(const std::string &msg);
 
 }  // namespace fsb
 
+namespace fsb {
+// staging of fs_encode_host (fsb_io.cpp): two library streams, their events, device buffers
+struct IoCache {
+  int device = -1;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
+  uint8_t *buf = nullptr;
+  uint64_t bytes = 0;
+  ~IoCache();
+};
+fs_status encode_host(const Graph &g, IoCache &c, uint32_t S, const uint8_t *h_data, uint64_t data_stride,
+                      uint8_t *h_checks, uint64_t checks_stride, uint8_t *h_coded, uint64_t coded_stride,
+                      uint32_t chunks, void *stream, uint32_t *launches);
+}  // namespace fsb
+
 struct fs_graph {
   fsb::Graph g;
+  std::mutex io_mu;                        // fs_encode_host staging (created on first use)
+  std::unique_ptr<fsb::IoCache> io;
 };
 
 // ------------------------------------------------------------------ decoder (NEXT-1, Alg 5)

@@ -27,7 +27,7 @@ EXPORTS = ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get
            "fs_decode_plan_free", "fs_encode_range", "fs_checks_create", "fs_checks_from_data",
            "fs_checks_data", "fs_checks_info_get", "fs_checks_free", "fs_repair_plan_create",
            "fs_repair_plan_info", "fs_repair_plan_rows", "fs_repair", "fs_repair_plan_free",
-           "fs_graph_extend")
+           "fs_graph_extend", "fs_encode_host")
 
 
 class FsError(RuntimeError):
@@ -97,6 +97,8 @@ def lib():
         L.fs_encode_range.argtypes = [P, P, P, P, u32, u32, u64, u64, P]
         L.fs_encode_range.restype = ctypes.c_int
         L.fs_encode_stripes.argtypes = [P, u32, P, u64, P, u64, P, u64, P]
+        L.fs_encode_host.argtypes = [P, u32, P, u64, P, u64, P, u64, u32, P]
+        L.fs_encode_host.restype = ctypes.c_int
         L.fs_graph_schedule.argtypes = [P, PP, ctypes.POINTER(u64), ctypes.POINTER(u32), PP,
                                         ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u32)]
         for f in ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get_info",
@@ -280,6 +282,20 @@ class Graph:
         t = self.t
         _check(lib().fs_encode_stripes(self._h, S, _ptr(data), self.k * t, _ptr(checks), self.p * t,
                                        _ptr(coded), self.n * t, _stream(stream)))
+
+    def encode_host(self, data, checks, coded, chunks=0, stream=None):
+        """fs_encode_host over contiguous [S,k,t] / [S,p,t] / [S,n,t] uint8 CPU tensors (pinned for
+        overlap): the library stages them through its own device buffers.  Asynchronous on
+        `stream` (the current stream by default): synchronise it before using the outputs."""
+        for x in (data, checks, coded):
+            if x is not None and (x.is_cuda or not x.is_contiguous()):
+                raise ValueError("encode_host takes contiguous host tensors")
+        S = data.shape[0]
+        t = self.t
+        _check(lib().fs_encode_host(self._h, S, ctypes.c_void_p(data.data_ptr()), self.k * t,
+                                    ctypes.c_void_p(checks.data_ptr()) if checks is not None else None,
+                                    self.p * t, ctypes.c_void_p(coded.data_ptr()), self.n * t, chunks,
+                                    _stream(stream)))
 
     def encode_stripes_raw(self, S, data_ptr, data_stride, checks_ptr, checks_stride, coded_ptr,
                            coded_stride, stream=None):

@@ -137,6 +137,10 @@ def test_host_only_graph_refuses_encode():
     st = fsb.lib().fs_encode(g._h, ctypes.c_void_p(16), None, ctypes.c_void_p(16), 0, 1, None)
     assert st == fsb.FS_EUNSUPPORTED
     assert b"host-only" in fsb.lib().fs_last_error()
+    buf = (ctypes.c_uint8 * 64)()
+    st = fsb.lib().fs_encode_host(g._h, 1, buf, 0, None, 0, buf, 0, 0, None)
+    assert st == fsb.FS_EUNSUPPORTED
+    assert fsb.lib().fs_encode_host(None, 1, buf, 0, None, 0, buf, 0, 0, None) == fsb.FS_EINVAL
 
 
 def test_schedule_balance():

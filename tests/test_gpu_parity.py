@@ -424,3 +424,33 @@ def test_smem_paired_and_unpaired_tiles(t, S):
     _, c, y = _run(cfg, fsb.VARIANT_SMEM, data=torch.from_numpy(D).cuda())
     _assert_equal(c, C, "checks t=%d" % t)
     _assert_equal(y, Y, "coded t=%d" % t)
+
+
+@pytest.mark.parametrize("cid,S,chunks,pinned", [(4, 6, 0, True), (4, 7, 3, True), (4, 5, 1, False),
+                                                 (5, None, 8, True), (5, None, 3, True), (3, None, 0, True),
+                                                 (2, None, 4, False), (1, None, 0, True)])
+def test_encode_host_matches_oracle(cid, S, chunks, pinned):
+    """fs_encode_host: host buffers staged through the library's device buffers, chunked by
+    stripes (S > 1) or by byte columns (one stripe), on two library streams -- every output byte
+    equals the oracle's; repeated calls with another chunking reuse the staging."""
+    _need_gpu()
+    cfg = configs.get(cid)
+    S = cfg["stripes"] if S is None else S
+    D, C, Y = _oracle_case(cfg, S)
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    g = fsb.Graph.create(cfg)
+    h_d = torch.from_numpy(D).contiguous()
+    if pinned:
+        h_d = h_d.pin_memory()
+    h_c = torch.full((S, p, t), 0xA5, dtype=torch.uint8, pin_memory=pinned) if p else None
+    h_y = torch.full((S, n, t), 0x5A, dtype=torch.uint8, pin_memory=pinned)
+    for ch in (chunks, 2):
+        g.encode_host(h_d, h_c, h_y, chunks=ch)
+        torch.cuda.synchronize()
+        if p:
+            _assert_equal(h_c.numpy(), C, "host checks (chunks=%d)" % ch)
+        _assert_equal(h_y.numpy(), Y, "host coded (chunks=%d)" % ch)
+        h_y.fill_(0x5A)
+        if p:
+            h_c.fill_(0xA5)
+    assert fsb.last_launch_count() >= 1
