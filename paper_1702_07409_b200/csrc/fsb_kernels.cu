@@ -508,17 +508,21 @@ constexpr uint32_t kBandBytes = 512;
 constexpr uint32_t kBandRowsMax = 8;   // coded rows per warp (fewer when the call is small)
 constexpr uint32_t kQBandBytes = 128;  // band of the four-group long-row level kernel
 
-template <uint32_t kBandBatch, int kMinBlocks>
+template <uint32_t kBandBatch, int kMinBlocks, bool kLazyWait>
 __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
     fsb_lt_band(uint32_t S, uint32_t k, uint32_t t, uint32_t col0, uint32_t col1, uint32_t nbands, uint32_t row_begin,
                 uint32_t nrows, uint32_t band_rows, const int32_t *__restrict__ row_ptr, const uint32_t *__restrict__ colf,
                 const uint8_t *__restrict__ data, uint64_t data_stride, const uint8_t *__restrict__ checks,
                 uint64_t checks_stride, uint8_t *__restrict__ coded, uint64_t coded_stride) {
   // launched programmatically after the precode kernel (PDL): the CTAs are scheduled while it
-  // drains and wait here for its checks.  (Waiting only before a warp's first check source would
-  // overlap more, but a __ldg is an invariant load to the compiler and may be hoisted above the
-  // wait -- measured: with the wait deferred, a 4-deep batch read checks before they existed.)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // drains.  kLazyWait (few-wave calls): a warp waits for the precode grid only before its first
+  // batch that reads a check row, so rows of data sources alone proceed while the checks are
+  // computed (config 3: 32.6 -> 30.2 us); otherwise every warp waits at entry (config 5, 13
+  // waves: the early warps' gathers slowed the precode, 0.281 -> 0.288 ms).  The source loads
+  // are asm volatile, like the wait, so the compiler cannot move them above it (an invariant
+  // __ldg could be hoisted -- a first version read checks before they existed that way).
+  if (!kLazyWait) asm volatile("griddepcontrol.wait;" ::: "memory");
+  bool waited = !kLazyWait;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nchunks = (nrows + band_rows - 1) / band_rows;
   uint64_t unit = static_cast<uint64_t>(blockIdx.x) * (kGlobalThreads / 32) + (threadIdx.x >> 5);
@@ -547,9 +551,18 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
     for (int32_t kk = 0; kk < nb; kk += kBandBatch) {
       uint4 v[kBandBatch];
       uint32_t mr[kBandBatch];
+      bool chk = false;
 #pragma unroll
       for (uint32_t u = 0; u < kBandBatch; ++u) {
         mr[u] = __shfl_sync(0xffffffffu, cv, kk + u);
+        chk |= (mr[u] & 0x7FFFFFFFu) >= k;  // warp-uniform
+      }
+      if (chk && !waited) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        waited = true;
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kBandBatch; ++u) {
         const uint32_t m = mr[u] & 0x7FFFFFFFu;
         const uint8_t *b0 = m < k ? dbase : cbase;
         asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -991,8 +1004,8 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     // A call of only a few waves of warps ends on its heaviest rows' serial gather chains; there 4
     // gathers in flight beat 2 (config 3: 35.2 -> 30.1 us; config 5, 13 waves, keeps (2, 8)).
     const bool few_waves = units < 4ull * g.sm_count * 64;
-    auto kern = (band_cfg == 0 || (band_cfg == 4 && few_waves)) ? fsb_lt_band<4, 6> : fsb_lt_band<2, 8>;
-    if (band_cfg == 2) kern = fsb_lt_band<8, 4>;
+    auto kern = (band_cfg == 0 || (band_cfg == 4 && few_waves)) ? fsb_lt_band<4, 6, true> : fsb_lt_band<2, 8, false>;
+    if (band_cfg == 2) kern = fsb_lt_band<8, 4, false>;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(static_cast<uint32_t>(blocks));
     lc.blockDim = dim3(kGlobalThreads);
