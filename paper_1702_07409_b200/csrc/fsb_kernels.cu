@@ -319,13 +319,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
 
-  if (threadIdx.x == 0) {
+  if (warp == kConsumerWarps && lane == 0) {
+    // the TMA thread: barriers, then -- once the previous grid in the stream has completed (this
+    // prologue may overlap its tail: programmatic dependent launch) -- tile 0's loads, issued
+    // while the other threads stage the schedule
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&full[b]), 1);
       mbar_init(smem_u32(&ready[b]), 1);
       mbar_init(smem_u32(&empty[b]), kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    uint32_t stripe, slice;
+    if (tile_of(a, 0, stripe, slice)) {  // buffer 0 is free: no wait on `empty`
+      if (a.debug & 1) {
+        mbar_arrive(smem_u32(&full[0]));
+      } else {
+        mbar_arrive_expect_tx(smem_u32(&full[0]), a.data_units * kUnitBytes);
+        for (uint32_t u = 0; u < a.data_units; ++u)
+          tma_load_3d(smem_base + u * kUnitBytes, &tmap, smem_u32(&full[0]), static_cast<int32_t>(slice * kSliceBytes),
+                      static_cast<int32_t>(u * kUnitRows), static_cast<int32_t>(stripe));
+      }
+    }
   }
   // the schedule (identical for every tile) and the two zero rows of each buffer
   for (uint32_t x = threadIdx.x; x < a.sched_chunks * (kChunkBytes / 16); x += blockDim.x)
@@ -338,13 +354,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // every thread past this point reads or writes user buffers after the previous grid is done;
+  // the next launch may then start its prologue on SMs as they free up
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == kConsumerWarps) {
     // ---------------------------------------------------------------- TMA warp (one lane)
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       uint32_t stripe, slice;
-      for (uint32_t i = 0; tile_of(a, i, stripe, slice); ++i) {
+      for (uint32_t i = 1; tile_of(a, i, stripe, slice); ++i) {  // tile 0: issued above
         const uint32_t b = i & 1, ph = (i >> 1) & 1;
         const uint32_t buf = smem_base + b * buf_bytes;
         mbar_wait(smem_u32(&empty[b]), ph ^ 1);  // consumers released tile i-2
@@ -958,8 +977,19 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
       a.wait_ns = wns;
     }
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(a.paired ? tiles / 2 : tiles, g.sm_count));
-    fsb_smem_encode<<<grid, kThreads, g.smem_bytes, stream>>>(tmap, a);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fsb_smem_encode launch");
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = g.smem_bytes;
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = pdl_enabled() ? 1 : 0;  // the prologue may overlap the previous grid's tail
+    e = cudaLaunchKernelEx(&lc, fsb_smem_encode, tmap, a);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "fsb_smem_encode launch");
     *launches = 1;
     return FS_OK;
   }
