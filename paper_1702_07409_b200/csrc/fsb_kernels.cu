@@ -344,8 +344,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   // the schedule (identical for every tile) and the two zero rows of each buffer
-  for (uint32_t x = threadIdx.x; x < a.sched_chunks * (kChunkBytes / 16); x += blockDim.x)
-    sts128(smem_u32(sched_s) + x * 16, __ldg(a.sched + x));
+  {  // 4 loads in flight per thread, then their stores (the copy is on every launch's critical path)
+    const uint32_t nx = a.sched_chunks * (kChunkBytes / 16);
+    for (uint32_t x0 = threadIdx.x; x0 < nx; x0 += 4 * blockDim.x) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t x = x0 + u * blockDim.x;
+        if (x < nx) v[u] = __ldg(a.sched + x);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t x = x0 + u * blockDim.x;
+        if (x < nx) sts128(smem_u32(sched_s) + x * 16, v[u]);
+      }
+    }
+  }
   for (uint32_t x = threadIdx.x; x < pre_n; x += blockDim.x) pre_s[x] = __ldg(&a.pre_slots[x]);
   if (threadIdx.x < 2 * 2 * (kSliceBytes / 16)) {  // 2 buffers x 2 rows x 4 lanes
     const uint32_t b = threadIdx.x >> 3, r = (threadIdx.x >> 2) & 1, l4 = threadIdx.x & 3;
