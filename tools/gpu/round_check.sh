@@ -28,3 +28,4 @@ for op in decode repair update; do
   timeout 300 python bench.py --op $op --steps 200 > $OUT/bench_$op.json 2> $OUT/bench_$op.err; cat $OUT/bench_$op.json
 done
 python tools/gpu/partition_share.py 5 200 > $OUT/partition_share.json 2>&1
+python tools/gpu/stripe_share.py 300 > $OUT/stripe_share.json 2>&1; cat $OUT/stripe_share.json
