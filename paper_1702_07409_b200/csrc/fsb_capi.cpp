@@ -548,6 +548,7 @@ uint32_t fs_last_launch_count(void) { return fsb::g_launches; }
 
 void fs_free(fs_graph *h) {
   if (!h) return;
+  h->io.reset();  // synchronises the fs_encode_host streams before the graph's device memory goes
   fsb::free_device(h->g);
   delete h;
 }
