@@ -454,3 +454,35 @@ def test_encode_host_matches_oracle(cid, S, chunks, pinned):
         if p:
             h_c.fill_(0xA5)
     assert fsb.last_launch_count() >= 1
+
+
+def test_encode_host_padded_strides_and_validation():
+    """fs_encode_host with host strides larger than the symbol block (stripes padded by 4 KiB):
+    the padding is neither read into the result nor written; strides below the minimum and NULL
+    buffers are rejected with FS_EINVAL."""
+    _need_gpu()
+    import ctypes
+    cfg = configs.get(4)
+    S = 3
+    D, C, Y = _oracle_case(cfg, S)
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    g = fsb.Graph.create(cfg)
+    pad = 4096
+    ds, cs, ys = k * t + pad, p * t + pad, n * t + pad
+    h_d = torch.full((S, ds), 0x33, dtype=torch.uint8).pin_memory()
+    h_c = torch.full((S, cs), 0xA5, dtype=torch.uint8).pin_memory()
+    h_y = torch.full((S, ys), 0x5A, dtype=torch.uint8).pin_memory()
+    h_d[:, :k * t] = torch.from_numpy(D.reshape(S, -1))
+    L = fsb.lib()
+    st = torch.cuda.current_stream()
+    ptr = lambda x: ctypes.c_void_p(x.data_ptr())
+    s = ctypes.c_void_p(st.cuda_stream)
+    assert L.fs_encode_host(g._h, S, ptr(h_d), ds, ptr(h_c), cs, ptr(h_y), ys, 2, s) == fsb.FS_OK
+    torch.cuda.synchronize()
+    _assert_equal(h_y[:, :n * t].numpy().reshape(S, n, t), Y, "coded (padded strides)")
+    _assert_equal(h_c[:, :p * t].numpy().reshape(S, p, t), C, "checks (padded strides)")
+    assert (h_y[:, n * t:] == 0x5A).all() and (h_c[:, p * t:] == 0xA5).all()
+    assert L.fs_encode_host(g._h, S, ptr(h_d), k * t - 16, ptr(h_c), cs, ptr(h_y), ys, 2, s) == fsb.FS_EINVAL
+    assert L.fs_encode_host(g._h, S, ptr(h_d), ds, None, cs, ptr(h_y), ys, 2, s) == fsb.FS_EINVAL
+    assert L.fs_encode_host(g._h, S, ptr(h_d), ds, ptr(h_c), cs, None, ys, 2, s) == fsb.FS_EINVAL
+    assert L.fs_encode_host(g._h, 0, None, 0, None, 0, None, 0, 0, s) == fsb.FS_OK
