@@ -186,7 +186,7 @@ FSB_API fs_status fs_encode_stripes(const fs_graph *g, uint32_t num_stripes,
 /* fs_encode_stripes with the buffers in HOST memory: the library stages them through device
  * memory it owns (allocated on first use, kept with g, freed by fs_free) and overlaps the copies
  * in both directions with the kernels, in `chunks` pieces (0 = 32) issued alternately on two
- * library streams: whole stripes when num_stripes > 1, byte columns (>= 1 KB, the
+ * library streams: whole stripes when num_stripes > 1, byte columns (>= 2 KB, the
  * fs_encode_range partition) for a single stripe.  Strides as for fs_encode_stripes (host
  * layout [stripe][symbol][t]; for one stripe the symbols are contiguous, stride t).  Host
  * buffers should be page-locked (cudaHostAlloc / cudaHostRegister) for the copies to overlap;

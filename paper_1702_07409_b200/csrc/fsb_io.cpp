@@ -4,7 +4,7 @@
 // library-owned streams:
 //   - several stripes (stripes are independent): chunks of whole stripes, one
 //     strided 2D copy per buffer and direction, fs_encode_stripes semantics per chunk;
-//   - one stripe: chunks of byte columns (>= 1 KB; XOR is bytewise, so a column range of the
+//   - one stripe: chunks of byte columns (>= 2 KB; XOR is bytewise, so a column range of the
 //     output depends only on the same columns of the input -- the fs_encode_range partition),
 //     2D copies of the column block of every row.
 // The staging buffers live with the graph (grown on demand, freed by fs_free).
@@ -62,7 +62,9 @@ fs_status encode_host(const Graph &g, IoCache &c, uint32_t S, const uint8_t *h_d
   uint64_t cw = 0;  // column chunk width (one stripe)
   uint32_t cs = 0;  // stripes per chunk
   if (S == 1) {
-    const uint64_t max_chunks = std::max<uint64_t>(1, t / 1024);
+    // >= 2 KB per row and chunk: the 2D copies' DMA rate drops with shorter rows (config 5, one
+    // box: 4 chunks of 2 KB 11.4 ms per step, 8 of 1 KB 12.0, 2 of 4 KB 13.4)
+    const uint64_t max_chunks = std::max<uint64_t>(1, t / 2048);
     nch = static_cast<uint32_t>(std::min<uint64_t>(chunks, max_chunks));
     cw = (t / nch + 63) / 64 * 64;  // 64-B slices keep the SMEM variant eligible
     nch = static_cast<uint32_t>((t + cw - 1) / cw);
