@@ -486,3 +486,27 @@ def test_encode_host_padded_strides_and_validation():
     assert L.fs_encode_host(g._h, S, ptr(h_d), ds, None, cs, ptr(h_y), ys, 2, s) == fsb.FS_EINVAL
     assert L.fs_encode_host(g._h, S, ptr(h_d), ds, ptr(h_c), cs, None, ys, 2, s) == fsb.FS_EINVAL
     assert L.fs_encode_host(g._h, 0, None, 0, None, 0, None, 0, 0, s) == fsb.FS_OK
+
+
+def test_encode_host_orders_after_stream_work():
+    """fs_encode_host starts after the work already queued on the caller's stream: the input host
+    buffer is filled by a device-to-host copy enqueued just before the call (behind a slow kernel),
+    and the encode must see the copied bytes, not the stale ones."""
+    _need_gpu()
+    cfg = configs.get(2)
+    D, C, Y = _oracle_case(cfg, 1)
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    g = fsb.Graph.create(cfg)
+    h_d = torch.zeros((1, k, t), dtype=torch.uint8).pin_memory()          # stale input
+    h_c = torch.empty((1, p, t), dtype=torch.uint8).pin_memory()
+    h_y = torch.empty((1, n, t), dtype=torch.uint8).pin_memory()
+    d_src = torch.from_numpy(D).cuda()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(20_000_000)                                      # keep the stream busy
+        h_d.copy_(d_src, non_blocking=True)                                # the real input
+        g.encode_host(h_d, h_c, h_y, chunks=2, stream=s)
+    s.synchronize()
+    _assert_equal(h_y.numpy(), Y, "coded after stream-ordered input")
+    _assert_equal(h_c.numpy(), C, "checks after stream-ordered input")
