@@ -510,3 +510,22 @@ def test_encode_host_orders_after_stream_work():
     s.synchronize()
     _assert_equal(h_y.numpy(), Y, "coded after stream-ordered input")
     _assert_equal(h_c.numpy(), C, "checks after stream-ordered input")
+
+
+@pytest.mark.parametrize("t,S,p,chunks", [(1040, 1, 8, 4), (8208, 1, 8, 8), (512, 5, 0, 2), (4160, 3, 4, 0)])
+def test_encode_host_ragged_sizes(t, S, p, chunks):
+    """fs_encode_host on sizes off the common grid: t not a multiple of 64 (one stripe: column
+    chunks end off a slice boundary, the GLOBAL variant), no precode with several stripes, and an
+    odd slice count; every byte against the oracle."""
+    _need_gpu()
+    cfg = dict(configs.get(2), k=300, p=p, d_p=3 if p else 0, n=390, t=t, stripes=S, seed=77 + t + S)
+    D, C, Y = _oracle_case(cfg, S)
+    g = fsb.Graph.create(cfg)
+    h_d = torch.from_numpy(D).contiguous().pin_memory()
+    h_c = torch.full((S, p, t), 0xA5, dtype=torch.uint8).pin_memory() if p else None
+    h_y = torch.full((S, cfg["n"], t), 0x5A, dtype=torch.uint8).pin_memory()
+    g.encode_host(h_d, h_c, h_y, chunks=chunks)
+    torch.cuda.synchronize()
+    _assert_equal(h_y.numpy(), Y, "coded")
+    if p:
+        _assert_equal(h_c.numpy(), C, "checks")
