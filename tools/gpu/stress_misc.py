@@ -1,6 +1,7 @@
 """Stress test on random small codes: fs_encode_range over random row x column blocks, the
-inactivation-completed decode, and repair with the library's check data -- every result against
-the oracle (encode bytes, BP + Gauss-Jordan decode bytes, repair plan replayed by the oracle).
+inactivation-completed decode, repair with the library's check data, and fs_encode_host (random
+stripe and chunk counts) -- every result against the oracle (encode bytes, BP + Gauss-Jordan
+decode bytes, repair plan replayed by the oracle).
 
     python tools/gpu/stress_misc.py FIRST_SEED END_SEED
 """
@@ -15,8 +16,8 @@ import torch  # noqa: E402
 import oracle  # noqa: E402
 from paper_1702_07409_b200 import configs, fsb, inputs  # noqa: E402
 
-bad = {"range": 0, "decode": 0, "repair": 0}
-ran = {"range": 0, "decode": 0, "repair": 0}
+bad = {"range": 0, "decode": 0, "repair": 0, "host": 0}
+ran = {"range": 0, "decode": 0, "repair": 0, "host": 0}
 for seed in range(int(sys.argv[1]), int(sys.argv[2])):
     rng = np.random.default_rng(31000 + seed)
     k = int(rng.integers(1, 300))
@@ -80,4 +81,24 @@ for seed in range(int(sys.argv[1]), int(sys.argv[2])):
     bad["repair"] += 0 if ok else 1
     if not ok:
         print("REPAIR mismatch", seed)
+    # fs_encode_host: random stripe count and chunking, host buffers (pinned or not)
+    S2 = int(rng.integers(1, 6))
+    c2 = dict(cfg, stripes=S2)
+    D2 = inputs.stripe_data(c2).numpy()
+    C2, Y2 = oracle.encode(go, D2)
+    pin = bool(rng.integers(0, 2))
+    hd = torch.from_numpy(D2).contiguous()
+    hd = hd.pin_memory() if pin else hd
+    hc = torch.full((S2, p, t), 0xA5, dtype=torch.uint8) if p else None
+    hy = torch.full((S2, n, t), 0x5A, dtype=torch.uint8)
+    if pin:
+        hc = hc.pin_memory() if p else None
+        hy = hy.pin_memory()
+    g.encode_host(hd, hc, hy, chunks=int(rng.integers(0, 9)))
+    torch.cuda.synchronize()
+    ok = np.array_equal(hy.numpy(), Y2) and (not p or np.array_equal(hc.numpy(), C2))
+    ran["host"] += 1
+    bad["host"] += 0 if ok else 1
+    if not ok:
+        print("HOST mismatch", seed, S2)
 print("done:", {key: "%d/%d bad" % (bad[key], ran[key]) for key in ran})
