@@ -312,7 +312,7 @@ void or_encode_stripes(uint32_t S, uint32_t k, uint32_t p, uint32_t n, uint64_t 
  * Pass A = Algorithm 1 on the LT survivors: sweep the surviving coded
  * symbols g = 0..; after zeroing the rows of recovered symbols, a column of weight 1
  * recovers its remaining neighbour.  Pass B = the same rule on the precode checks
- * ("BP ... at most twice").  Reading (R19): A and B alternate until
+ * ("BP ... at most twice").  Reading (R22): A and B alternate until
  * neither recovers anything.  Then, if use_elim, GF(2) Gauss-Jordan elimination on the
  * residual system recovers every symbol the received equations determine.
  * out_I: K*t bytes.  state[m]: 0 unrecovered, 1 recovered by BP, 2 recovered by elimination.

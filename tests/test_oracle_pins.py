@@ -468,6 +468,41 @@ def test_decoder_peeling_only_matches_alg1_closure():
     assert not state.any()
 
 
+def _peel_tool():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "decode_readings", os.path.join(os.path.dirname(__file__), "..", "tools", "decode_readings.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+@pytest.mark.parametrize("cid,frac", [(1, 1.0), (2, 0.95), (3, 1.0), (4, 1.0), (4, 0.9)])
+def test_decoder_bp_set_is_the_union_peeling_closure(cid, frac):
+    """Reading R22: the oracle's BP (passes A and B alternated) recovers exactly
+    the peeling closure of {received LT equations} U {precode equations} -- checked against an
+    independent queue-based peeling (tools/decode_readings.py, graph only; the closure is the
+    same whatever the visiting order).  The literal reading (LT BP to its fixpoint, then one
+    precode BP) recovers a subset of it (profiles/r02/decode_readings.jsonl: equal on configs
+    1-4, 1-2 symbols fewer on config 5)."""
+    tool = _peel_tool()
+    g = oracle.generate_graph(configs.get(cid))
+    recv = np.ones(g.n, bool) if frac == 1.0 else np.random.default_rng(cid).random(g.n) < frac
+    t = 16
+    Y = np.zeros((g.n, t), np.uint8)
+    _, state = oracle.decode(dict_graph_t(g, t), recv, Y, use_elim=False)
+    union = tool.union_fixpoint(g, recv)
+    assert np.array_equal(state != 0, union)
+    lit = tool.literal_two_pass(g, recv)
+    assert not np.any(lit & ~union)
+
+
+def dict_graph_t(g, t):
+    """The same graph with symbol size t (the recovered SET does not depend on t)."""
+    cfg = dict(k=g.k, p=g.p, n=g.n, t=t)
+    return oracle.Graph(cfg, g.pre_row_ptr, g.pre_col, g.lt_row_ptr, g.lt_col)
+
+
 def test_paper_repair_example_xor_algebra():
     """P11 (off-path, XOR algebra only): Eqs (1)-(3) with the check #1 group
     (D0, D1, D2) give Eq (4): C2 ^ C12 ^ C17 ^ C20 ^ C21 = D0 ^ D1 ^ D2.  Checked on random
@@ -508,6 +543,44 @@ def test_array_precode_golden_k6_b3():
     want = [[int(r[1])] for r in _golden_rows("array_ldpc_k6_b3.txt")]
     got = [col[rp[i]:rp[i + 1]].tolist() for i in range(3)]
     assert got == want
+
+
+def _golden_members(name):
+    return [[int(x) for x in r[1:]] for r in _golden_rows(name)]
+
+
+def test_array_precode_golden_k15_K25():
+    """tests/golden/array_ldpc_k15_K25.txt: Alg 2 evaluated by hand at a shape
+    where every term of the index formula is live: j' = 2, so block row 0 has the slope
+    m(j'-j-1) = m, and block row 1 reads the checks of block row 0 (R18)."""
+    rp, col = oracle.array_precode(15, 25)
+    want = _golden_members("array_ldpc_k15_K25.txt")
+    assert len(rp) == 11
+    got = [col[rp[i]:rp[i + 1]].tolist() for i in range(10)]
+    assert got == want
+
+
+def _alg2_variant(b, K, slope_shift=-1, offset_shift=-1):
+    """Alg 2's index formula with the two '-1' terms of PAPER.md:180 made parameters, for the
+    mutation check below only (never used to pin the oracle):
+    l = k'P - (j'-j+m-1)P - ((m(j'-j+slope_shift) - i + offset_shift + P) mod P) - 1."""
+    P = _lpf(K)
+    kp, jp = K // P, K // P - b // P
+    return [[kp * P - (jp - j + m - 1) * P - ((m * (jp - j + slope_shift) - i + offset_shift + P) % P) - 1
+             for m in range(1, kp - jp + 1)] for j in range(jp) for i in range(P)]
+
+
+def test_array_precode_golden_rejects_formula_slips():
+    """The k15/K25 golden is discriminating: plausible transcription slips of PAPER.md:180 --
+    the slope m(j'-j) instead of m(j'-j-1), or '- i' without the '- 1' -- change rows of it (so
+    an oracle carrying either slip fails test_array_precode_golden_k15_K25), while the formula
+    as printed reproduces it."""
+    want = _golden_members("array_ldpc_k15_K25.txt")
+    assert _alg2_variant(15, 25) == want
+    slope = _alg2_variant(15, 25, slope_shift=0)
+    assert sum(a != b for a, b in zip(slope, want)) == 10  # every row moves
+    off = _alg2_variant(15, 25, offset_shift=0)
+    assert off != want
 
 
 @pytest.mark.parametrize("k,K", ARRAY_CASES)

@@ -110,16 +110,37 @@ def test_cga_invariants(i):
             assert np.array_equal(acc, I[x])
 
 
-def test_cga_converges_on_omega_configs():
-    """The paper's claim holds on the Omega(x) configs: n-K zero columns, every
-    symbol with exactly one Group #2 set."""
-    for cid in (2,):
-        g = fsb.Graph.create(configs.get(cid), host_only=True)
-        ch = fsb.Checks.create(g)
-        inf = ch.info()
-        assert inf["zero_columns"] >= g.n - g.K and inf["weight1_columns"] == g.K
-        xs = [x for kind, x, _ in oracle.parse_check_data(ch.data()) if kind == 2]
-        assert sorted(xs) == list(range(g.K))
+def test_cga_converges_on_full_rank_c2():
+    """The paper's claim (CGA converges whenever B has full rank) on config 2 (RSD
+    c=0.05, B of full rank): n-K zero columns and every symbol with exactly one Group #2 set
+    (PAPER.md:315)."""
+    g = fsb.Graph.create(configs.get(2), host_only=True)
+    inf = fsb.Checks.create(g).info()
+    assert inf["zero_columns"] >= g.n - g.K and inf["weight1_columns"] == g.K
+    xs = [x for kind, x, _ in oracle.parse_check_data(fsb.Checks.create(g).data()) if kind == 2]
+    assert sorted(xs) == list(range(g.K))
+
+
+def test_cga_on_omega_config3():
+    """Config 3 is the Omega(x) code.  Its B is NOT of full rank (8 of the
+    10,100 symbols are in no LT row; the column space of B determines 10,091 symbols -- oracle
+    GF(2) elimination), so PAPER.md:265's premise fails.  CGA still reaches Alg 4's exit test
+    (zero_columns >= n-K, reading R19), every Group #2 symbol is one B determines, and the
+    Group #2 sets cover all but 5 of the determined symbols."""
+    c = configs.get(3)
+    g = fsb.Graph.create(c, host_only=True)
+    ch = fsb.Checks.create(g)
+    inf = ch.info()
+    assert inf["zero_columns"] >= g.n - g.K
+    go = oracle.generate_graph(c)
+    gg = oracle.Graph(dict(k=go.K, p=0, n=go.n, t=8), np.zeros(1, np.int32), np.zeros(0, np.int32),
+                      go.lt_row_ptr, go.lt_col)
+    _, st = oracle.decode(gg, np.ones(go.n, bool), np.zeros((go.n, 8), np.uint8))
+    det = set(np.nonzero(st)[0].tolist())
+    xs = [x for kind, x, _ in oracle.parse_check_data(ch.data()) if kind == 2]
+    assert len(xs) == len(set(xs)) == inf["weight1_columns"]
+    assert set(xs) <= det
+    assert len(det) == 10091 and len(xs) == 10086
 
 
 @pytest.mark.parametrize("i", range(10))
