@@ -40,6 +40,17 @@ DATA = "synthetic: seeded counter-form splitmix64 bytes (DESIGN.md R4), graph se
 # Shared-memory gather peak for the secondary (gather-traffic) roofline: parity-paired 64-B row
 # gathers, 122 B/clk/SM at 1965 MHz x 148 SMs (tools/microbench/mb3.cu, profiles/r01b/).
 SMEM_GATHER_PEAK_GBS = 35595.0
+# L2-resident random 512-B row gathers from global memory (the GLOBAL variant's gathers hit L2):
+# 66.9 B/clk/SM at 1965 MHz x 148 SMs (tools/microbench/mb7.cu, profiles/r01e/mb7.txt).
+L2_GATHER_PEAK_GBS = 19500.0
+# The paper's own CPU numbers (context only, another machine): PAPER.md:452-475 (Table 1, encode)
+# and PAPER.md:486-489 (Table 2, decode), 2x Intel Xeon E5-2620 (12 threads), 64 MiB test file.
+PAPER_CONTEXT = {
+    "source": "PAPER.md:452-489 (§4, Tables 1-2); another machine, context only",
+    "hardware": "2x Intel Xeon E5-2620 (12 cores / 12 threads used), 2012-era",
+    "encode_MBps_best": 2722, "decode_MBps_best": 1691,
+    "note": "the paper's library, its own PRNG/graphs and a 64 MiB file: not the same workload",
+}
 REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
 
@@ -143,6 +154,30 @@ def plan(cfg, ws, rank, scaling, partition="rows"):
     return "stripes", a, b - a
 
 
+def workload_config(cfg, args, ws, kind, S, u0, u1, lt_nnz, max_degree):
+    """The `config` object of a bench line; the GPU arm and the reference arm emit the same one."""
+    k, p, n, t = cfg["k"], cfg["p"], cfg["n"], cfg["t"]
+    rows = n if kind != "rows" else u1 - u0
+    cols = u1 - u0 if kind == "cols" else t
+    work_bytes = S * (k + p + rows) * cols
+    flush = work_bytes < 2 * L2_BYTES
+    return {"workload": cfg["name"], "k": k, "p": p, "d_p": cfg["d_p"], "n": n, "t": t,
+            "dist": "RSD" if cfg["dist"] == configs.RSD else "Omega",
+            "stripes_total": cfg["stripes"] * (ws if args.scaling == "weak" and kind == "stripes" else 1),
+            "per_rank": {"stripes": "%d stripes" % S, "rows": "rows [%d,%d)" % (u0, u1),
+                         "cols": "bytes [%d,%d)" % (u0, u1)}[kind],
+            "parallelism": {"stripes": "stripe-sharded x%d" % ws,
+                            "rows": "coded-row partition x%d, source replicated" % ws,
+                            "cols": "byte-column partition x%d, nothing replicated" % ws}[kind],
+            "variant": args.variant,
+            "l2": ("working set %.1f MB per rank < 2x the 126 MB L2: a 252 MiB scratch write "
+                   "before each timed step (excluded), steps timed one by one" % (work_bytes / 1e6))
+                  if flush else
+                  ("working set (%.2f GB per rank) exceeds the 126 MB L2; steps back to back, no flush"
+                   % (work_bytes / 1e9)),
+            "lt_nnz": int(lt_nnz), "max_degree": int(max_degree)}
+
+
 def cpu_oracle_sample(cfg, seconds, max_stripes=None):
     """The oracle, as it stands (single-threaded C), on a bounded sample of the workload:
     whole stripes of the config until `seconds` of CPU work (at least one)."""
@@ -188,6 +223,16 @@ def cpu_oracle_sample_mt(cfg, seconds):
             "sample": "%d of %d stripes, %d threads, %.2f s" % (done, S, nthreads, t_enc)}
 
 
+def _reference_config(args, cfg, ws):
+    """The GPU arm's config object for the same launch (rank 0's share at this world size)."""
+    import numpy as np
+    import oracle
+    go = oracle.generate_graph(cfg)
+    kind, u0, u1 = plan(cfg, ws, 0, args.scaling, args.partition)
+    S = u1 if kind == "stripes" else 1
+    return workload_config(cfg, args, ws, kind, S, u0, u1, go.nnz, int(np.diff(go.lt_row_ptr).max()))
+
+
 def run_reference(args, cfg):
     """Reference arm for this tier: the CPU oracle timed as it stands on the host cores, on the
     same config, metric and unit; rank 0 only, the whole run bounded by --ref-seconds."""
@@ -211,9 +256,8 @@ def run_reference(args, cfg):
            "steps": steps, "warmup": warm, "ms_per_step": round(1e3 * statistics.median(secs), 3),
            "higher_is_better": True, "scaling": args.scaling,
            "vs_baseline": None, "dtype": "u8", "data": DATA,
-           "config": {"workload": cfg["name"], "k": cfg["k"], "p": cfg["p"], "n": cfg["n"],
-                      "t": cfg["t"], "stripes": cfg["stripes"]},
-           "cpu_baseline": cb,
+           "config": _reference_config(args, cfg, ws),
+           "cpu_baseline": cb, "context": PAPER_CONTEXT,
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
@@ -384,6 +428,14 @@ def main():
         except Exception:
             traffic = None
     smem_kernel = launches_per_step == 1
+    # the gathers of the SMEM kernel hit shared memory, those of the GLOBAL band kernel L2: each
+    # against its own builder-measured peak (microbenchmarks on this pool, not driver-measured)
+    if smem_kernel:
+        gpeak, gsrc = SMEM_GATHER_PEAK_GBS, ("builder-measured parity-paired 64-B smem row gather "
+                                             "(tools/microbench/mb3.cu, profiles/r01b)")
+    else:
+        gpeak, gsrc = L2_GATHER_PEAK_GBS, ("builder-measured L2-resident random 512-B row gather "
+                                           "(tools/microbench/mb7.cu, profiles/r01e/mb7.txt)")
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
             "algorithmic_bytes_per_launch": b_hbm, "peak_source": peak_src,
@@ -392,9 +444,9 @@ def main():
                       % (launches_per_step, "" if smem_kernel else "es"),
             "gather": {"bytes_per_launch": b_gather,
                        "achieved": round(b_gather / (launch_ms * 1e-3) / 1e9, 1),
-                       "peak": SMEM_GATHER_PEAK_GBS, "unit": "GB/s",
-                       "frac": round(b_gather / (launch_ms * 1e-3) / 1e9 / SMEM_GATHER_PEAK_GBS, 4),
-                       "peak_source": "measured parity-paired 64-B smem row gather, tools/microbench/mb3.cu"}}
+                       "peak": gpeak, "unit": "GB/s",
+                       "frac": round(b_gather / (launch_ms * 1e-3) / 1e9 / gpeak, 4),
+                       "peak_source": gsrc}}
 
     collectives = None
     if ws > 1:
@@ -418,22 +470,8 @@ def main():
            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
            "scaling": args.scaling if kind == "stripes" else "strong", "vs_baseline": None, "dtype": "u8",
            "data": DATA,
-           "config": {"workload": cfg["name"], "k": k, "p": p, "d_p": cfg["d_p"], "n": n, "t": t,
-                      "dist": "RSD" if cfg["dist"] == configs.RSD else "Omega",
-                      "stripes_total": cfg["stripes"] * (ws if args.scaling == "weak" and kind == "stripes" else 1),
-                      "per_rank": {"stripes": "%d stripes" % S, "rows": "rows [%d,%d)" % (u0, u1),
-                                   "cols": "bytes [%d,%d)" % (u0, u1)}[kind],
-                      "parallelism": {"stripes": "stripe-sharded x%d" % ws,
-                                      "rows": "coded-row partition x%d, source replicated" % ws,
-                                      "cols": "byte-column partition x%d, nothing replicated" % ws}[kind],
-                      "variant": args.variant,
-                      "l2": ("working set %.1f MB per rank < 2x the 126 MB L2: a 252 MiB scratch write "
-                             "before each timed step (excluded), steps timed one by one" % (work_bytes / 1e6))
-                            if flush else
-                            ("working set (%.2f GB per rank) exceeds the 126 MB L2; steps back to back, no flush"
-                             % (work_bytes / 1e9)),
-                      "lt_nnz": inf["lt_nnz"], "max_degree": inf["max_degree"]},
-           "roofline": roof, "gpu_launches": launches_per_step * args.steps,
+           "config": workload_config(cfg, args, ws, kind, S, u0, u1, inf["lt_nnz"], inf["max_degree"]),
+           "roofline": roof, "context": PAPER_CONTEXT, "gpu_launches": launches_per_step * args.steps,
            "step_ms_median": round(statistics.median(per), 5), "step_ms_best": round(min(per), 5),
            "clocks": clk, "e2e": e2e}
     if collectives:

@@ -277,8 +277,9 @@ fs_status validate_csr(const Graph &g) {
     for (uint32_t r = 0; r < rows; ++r) {
       if (rp[r + 1] < rp[r] || static_cast<size_t>(rp[r + 1]) > col.size()) return false;
       if (rp[r + 1] == rp[r]) return false;  // every row has degree >= 1
-      if (precode && g.prm.precode == FS_PRECODE_RANDOM && static_cast<uint32_t>(rp[r + 1] - rp[r]) != g.prm.d_p)
-        return false;
+      // every precode row has exactly d_p members whatever the precode kind: the kernels index
+      // member e of check c as pre_col[c*d_p + e] and size the staged member rows by p*d_p
+      if (precode && static_cast<uint32_t>(rp[r + 1] - rp[r]) != g.prm.d_p) return false;
       ++epoch;
       for (int32_t e = rp[r]; e < rp[r + 1]; ++e) {
         const int32_t m = col[e];
@@ -290,6 +291,13 @@ fs_status validate_csr(const Graph &g) {
     }
     return static_cast<size_t>(rp[rows]) == col.size();
   };
+  if (p && g.prm.precode == FS_PRECODE_ARRAY) {  // Alg 2's shape fixes the member count k'-j'
+    uint32_t P = 0, kp = 0, jp = 0;
+    if (!array_shape(k, K, P, kp, jp) || g.prm.d_p != kp - jp) {
+      set_error("array precode CSR: members per check must be k'-j' of Alg 2");
+      return FS_EINVAL;
+    }
+  }
   if (!check_rows(g.pre_row_ptr, g.pre_col, p, true)) { set_error("invalid precode CSR"); return FS_EINVAL; }
   if (!check_rows(g.lt_row_ptr, g.lt_col, n, false)) { set_error("invalid LT CSR"); return FS_EINVAL; }
   return FS_OK;
@@ -528,7 +536,9 @@ void build_smem_schedule(Graph &g) {
     per_warp[l.second].push_back(idx);
     heap.push({l.first + cost(items[idx]), l.second});
   }
+#ifdef FSB_EXPERIMENTS
   // profiling experiment (FSB_SCHED_DEBUG=zero): every slot reads a zero row of its half's parity
+  // -- output is wrong by design, so it exists only in experiment builds (-DFSB_EXPERIMENTS)
   if (const char *dbg = std::getenv("FSB_SCHED_DEBUG")) {
     if (std::string(dbg) == "zero")
       for (Item &it : items)
@@ -536,6 +546,7 @@ void build_smem_schedule(Graph &g) {
           for (int hh = 0; hh < 2; ++hh)
             for (uint16_t &v : it.grp[q].seq[hh]) v = hh ? z1 : z0;
   }
+#endif
   // emit the two chunk streams, warp after warp (32 words per chunk; half-group h: words 4h..4h+3)
   s.warp_info.assign(kConsumerWarps * 3, 0);
   std::vector<uint32_t> heads, conts;

@@ -73,8 +73,9 @@ fs_status encode_host(const Graph &g, IoCache &c, uint32_t S, const uint8_t *h_d
     nch = std::min(S, chunks);
     cs = (S + nch - 1) / nch;
     nch = (S + cs - 1) / cs;
-    need = 2ull * cs * rows * t;  // one set per stream
+    need = std::min<uint64_t>(nch, 2) * cs * rows * t;  // one set per stream in use
   }
+  const uint64_t set_bytes = static_cast<uint64_t>(cs) * rows * t;  // S > 1: one staging set
   // a new call starts after everything the previous one issued (its chunking may differ)
   for (int j = 0; j < 2; ++j) {
     if ((e = cudaStreamWaitEvent(c.st[j], c.done[0], 0)) != cudaSuccess) return io_fail(e, "cudaStreamWaitEvent");
@@ -93,7 +94,7 @@ fs_status encode_host(const Graph &g, IoCache &c, uint32_t S, const uint8_t *h_d
   if ((e = cudaEventRecord(c.start, stream)) != cudaSuccess) return io_fail(e, "cudaEventRecord");
   for (int j = 0; j < 2; ++j)
     if ((e = cudaStreamWaitEvent(c.st[j], c.start, 0)) != cudaSuccess) return io_fail(e, "cudaStreamWaitEvent");
-  for (uint32_t i = 0; i < nch; ++i) {
+  auto issue_chunk = [&](uint32_t i) -> fs_status {
     cudaStream_t st = c.st[i & 1];
     uint32_t L = 0;
     fs_status s;
@@ -110,7 +111,7 @@ fs_status encode_host(const Graph &g, IoCache &c, uint32_t S, const uint8_t *h_d
         return io_fail(e, "cudaMemcpy2DAsync (coded)");
     } else {
       const uint32_t a = i * cs, b = std::min(S, a + cs), m = b - a;
-      uint8_t *d = c.buf + (i & 1) * (need / 2), *ck = d + cs * k * t, *y = ck + cs * p * t;
+      uint8_t *d = c.buf + (i & 1) * set_bytes, *ck = d + cs * k * t, *y = ck + cs * p * t;
       if ((e = cudaMemcpy2DAsync(d, k * t, h_data + a * data_stride, data_stride, k * t, m, cudaMemcpyHostToDevice,
                                  st)) != cudaSuccess)
         return io_fail(e, "cudaMemcpy2DAsync (data)");
@@ -124,13 +125,18 @@ fs_status encode_host(const Graph &g, IoCache &c, uint32_t S, const uint8_t *h_d
         return io_fail(e, "cudaMemcpy2DAsync (coded)");
     }
     *launches += L;
-  }
-  // the caller's stream continues after both library streams
+    return FS_OK;
+  };
+  // every exit after this point first records done[] on both library streams and makes the
+  // caller's stream wait for them, so chunks already queued when a later one fails are ordered
+  // before anything the caller (or the next call) does with these buffers
+  fs_status status = FS_OK;
+  for (uint32_t i = 0; i < nch && status == FS_OK; ++i) status = issue_chunk(i);
   for (int j = 0; j < 2; ++j) {
     if ((e = cudaEventRecord(c.done[j], c.st[j])) != cudaSuccess) return io_fail(e, "cudaEventRecord");
     if ((e = cudaStreamWaitEvent(stream, c.done[j], 0)) != cudaSuccess) return io_fail(e, "cudaStreamWaitEvent");
   }
-  return FS_OK;
+  return status;
 }
 
 }  // namespace fsb

@@ -979,11 +979,17 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     }
     a.cont_base = g.sched.cont_base;
     {
+      // FSB_DEBUG experiments (1 = no TMA loads: wrong bytes by design; 2 = wait counters) exist
+      // only in experiment builds (-DFSB_EXPERIMENTS); a release build never reads the variable
+#ifdef FSB_EXPERIMENTS
       static const uint32_t dbg = [] {
         const char *e = std::getenv("FSB_DEBUG");
         return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
       }();
       a.debug = dbg;
+#else
+      a.debug = 0;
+#endif
       static const uint32_t wns = [] {
         const char *e = std::getenv("FSB_WAIT_NS");
         return e ? static_cast<uint32_t>(std::atoi(e)) : 500u;

@@ -10,7 +10,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfsb200.so")
+# FSB_LIB selects another build of the same sources (same-box A/B runs, tools/gpu/ab/run_ab.sh);
+# the default is the in-tree libfsb200.so that build() writes
+LIB_PATH = os.environ.get("FSB_LIB") or os.path.join(_HERE, "libfsb200.so")
 
 FS_OK, FS_EINVAL, FS_EDIST, FS_ENOMEM, FS_ECUDA, FS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 FS_DIST_RSD, FS_DIST_FINITE = 1, 2
@@ -160,6 +162,33 @@ def _ptr(x):
     return ctypes.c_void_p(x.data_ptr())
 
 
+def _buf(x, name, nbytes, cuda=True, optional=False):
+    """Pointer of a caller buffer after checking what the C ABI cannot (it only sees a raw
+    pointer): uint8 dtype, placement (CUDA tensor on the current device, or a host tensor),
+    contiguity and at least `nbytes` bytes -- an undersized tensor would otherwise be read or
+    written past its end by the kernels (or by the D2H copies of fs_encode_host)."""
+    import torch
+    if x is None:
+        if optional:
+            return None
+        raise ValueError("%s: a tensor is required" % name)
+    if x.dtype != torch.uint8:
+        raise ValueError("%s: expected dtype uint8, got %s" % (name, x.dtype))
+    if cuda:
+        if not x.is_cuda:
+            raise ValueError("%s: expected a CUDA tensor" % name)
+        if x.device.index != torch.cuda.current_device():
+            raise ValueError("%s: tensor on cuda:%d, current device is cuda:%d"
+                             % (name, x.device.index, torch.cuda.current_device()))
+    elif x.is_cuda:
+        raise ValueError("%s: expected a host tensor" % name)
+    if not x.is_contiguous():
+        raise ValueError("%s: expected a contiguous tensor" % name)
+    if x.numel() < nbytes:
+        raise ValueError("%s: expected %d bytes, got %d" % (name, nbytes, x.numel()))
+    return ctypes.c_void_p(x.data_ptr())
+
+
 def _stream(stream):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -268,33 +297,40 @@ class Graph:
     def encode(self, data, checks, coded, row_begin=0, row_end=None, stream=None):
         """fs_encode: one stripe, coded rows [row_begin, row_end) into `coded`."""
         row_end = self.n if row_end is None else row_end
-        _check(lib().fs_encode(self._h, _ptr(data), _ptr(checks), _ptr(coded), row_begin, row_end,
-                               _stream(stream)))
+        t = self.t
+        rows = max(int(row_end) - int(row_begin), 0)
+        _check(lib().fs_encode(self._h, _buf(data, "data", self.k * t), self._checks_ptr(checks, 1, True),
+                               _buf(coded, "coded", rows * t), row_begin, row_end, _stream(stream)))
+
+    def _checks_ptr(self, checks, S, cuda):
+        # None goes through: the library rejects a missing checks buffer when p > 0 (FS_EINVAL)
+        return _buf(checks, "checks", S * self.p * self.t, cuda=cuda, optional=True)
 
     def encode_range(self, data, checks, coded, row_begin, row_end, col_begin, col_end, stream=None):
         """fs_encode_range: rows [row_begin, row_end) and bytes [col_begin, col_end) of one stripe."""
-        _check(lib().fs_encode_range(self._h, _ptr(data), _ptr(checks), _ptr(coded), row_begin, row_end,
-                                     col_begin, col_end, _stream(stream)))
+        t = self.t
+        rows = max(int(row_end) - int(row_begin), 0)
+        _check(lib().fs_encode_range(self._h, _buf(data, "data", self.k * t), self._checks_ptr(checks, 1, True),
+                                     _buf(coded, "coded", rows * t), row_begin, row_end, col_begin, col_end,
+                                     _stream(stream)))
 
     def encode_stripes(self, data, checks, coded, stream=None):
         """fs_encode_stripes over contiguous [S,k,t] / [S,p,t] / [S,n,t] uint8 CUDA tensors."""
         S = data.shape[0]
         t = self.t
-        _check(lib().fs_encode_stripes(self._h, S, _ptr(data), self.k * t, _ptr(checks), self.p * t,
-                                       _ptr(coded), self.n * t, _stream(stream)))
+        _check(lib().fs_encode_stripes(self._h, S, _buf(data, "data", S * self.k * t), self.k * t,
+                                       self._checks_ptr(checks, S, True), self.p * t,
+                                       _buf(coded, "coded", S * self.n * t), self.n * t, _stream(stream)))
 
     def encode_host(self, data, checks, coded, chunks=0, stream=None):
         """fs_encode_host over contiguous [S,k,t] / [S,p,t] / [S,n,t] uint8 CPU tensors (pinned for
         overlap): the library stages them through its own device buffers.  Asynchronous on
         `stream` (the current stream by default): synchronise it before using the outputs."""
-        for x in (data, checks, coded):
-            if x is not None and (x.is_cuda or not x.is_contiguous()):
-                raise ValueError("encode_host takes contiguous host tensors")
         S = data.shape[0]
         t = self.t
-        _check(lib().fs_encode_host(self._h, S, ctypes.c_void_p(data.data_ptr()), self.k * t,
-                                    ctypes.c_void_p(checks.data_ptr()) if checks is not None else None,
-                                    self.p * t, ctypes.c_void_p(coded.data_ptr()), self.n * t, chunks,
+        _check(lib().fs_encode_host(self._h, S, _buf(data, "data", S * self.k * t, cuda=False), self.k * t,
+                                    self._checks_ptr(checks, S, False), self.p * t,
+                                    _buf(coded, "coded", S * self.n * t, cuda=False), self.n * t, chunks,
                                     _stream(stream)))
 
     def encode_stripes_raw(self, S, data_ptr, data_stride, checks_ptr, checks_stride, coded_ptr,
@@ -349,8 +385,8 @@ class DecodePlan:
         """fs_decode over contiguous [S,n,t] coded and [S,K,t] intermediate uint8 CUDA tensors."""
         S = coded.shape[0]
         t = self.graph.t
-        _check(lib().fs_decode(self._h, S, _ptr(coded), self.graph.n * t, _ptr(inter), self.graph.K * t,
-                               _stream(stream)))
+        _check(lib().fs_decode(self._h, S, _buf(coded, "coded", S * self.graph.n * t), self.graph.n * t,
+                               _buf(inter, "inter", S * self.graph.K * t), self.graph.K * t, _stream(stream)))
 
     def free(self):
         if self._h:
@@ -456,7 +492,8 @@ class RepairPlan:
         """fs_repair in place over contiguous [S,n,t] coded (and [S,K,t] inter) CUDA tensors."""
         S = coded.shape[0]
         t = self.graph.t
-        _check(lib().fs_repair(self._h, S, _ptr(coded), self.graph.n * t, _ptr(inter), self.graph.K * t,
+        _check(lib().fs_repair(self._h, S, _buf(coded, "coded", S * self.graph.n * t), self.graph.n * t,
+                               _buf(inter, "inter", S * self.graph.K * t, optional=True), self.graph.K * t,
                                _stream(stream)))
 
     def free(self):

@@ -70,10 +70,12 @@ def test_config_parity(cid, variant):
     _assert_equal(y, Y, "coded")
 
 
-def test_row_range_partition_concatenates():
-    """P10 / SURVEY §8(e): rows [r*n/G, (r+1)*n/G) per rank concatenate to the full output."""
+@pytest.mark.parametrize("cid", [3, 5])
+def test_row_range_partition_concatenates(cid):
+    """P10 / SURVEY §8(e): rows [r*n/G, (r+1)*n/G) per rank concatenate to the full output
+    (config 5: BASELINE.json:configs[5]'s coded-symbol range partition, reading R16)."""
     _need_gpu()
-    cfg = configs.get(3)
+    cfg = configs.get(cid)
     g = fsb.Graph.create(cfg)
     D, C, Y = _oracle_case(cfg)
     d = torch.from_numpy(D[0]).cuda()
