@@ -35,6 +35,7 @@
 
 #include "fsb_internal.h"
 
+
 namespace fsb {
 
 // --------------------------------------------------------------------------- PTX helpers
@@ -596,7 +597,10 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
       }
 #pragma unroll
       for (uint32_t u = 0; u < kBandBatch; ++u) {
-        const uint32_t m = mr[u] & 0x7FFFFFFFu;
+        uint32_t m = mr[u] & 0x7FFFFFFFu;
+#if defined(FSB_EXPERIMENTS) && defined(FSB_BAND_L2ONLY)
+        m &= 1023u;  // experiment: every gather L2-resident (wrong bytes by design)
+#endif
         const uint8_t *b0 = m < k ? dbase : cbase;
         asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
@@ -614,6 +618,118 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
         }
       }
     }
+  }
+}
+
+// The source address of marked edge f: data row m < k or check row m - k (cbase = checks - k*t).
+__device__ __forceinline__ const uint8_t *src_addr(uint32_t f, uint32_t k, uint32_t t, const uint8_t *dbase,
+                                                   const uint8_t *cbase) {
+  uint32_t m = f & 0x7FFFFFFFu;
+#if defined(FSB_EXPERIMENTS) && defined(FSB_BAND_L2ONLY)
+  m &= 1023u;  // experiment: every gather L2-resident (wrong bytes by design)
+#endif
+  return (m < k ? dbase : cbase) + static_cast<uint64_t>(m) * t;
+}
+__device__ __forceinline__ uint4 ldg16(const uint8_t *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+// fsb_lt_band4: the band kernel for many-wave calls (config 5).  Same units, band-major order and
+// marked CSR as fsb_lt_band; kB gathers per batch.  A chunk's edge count modulo kB is taken first
+// as one predicated partial batch, so every later batch issues kB unpredicated gathers, and row
+// ends inside a batch are found with one warp vote (the flags are warp-uniform).  Stores are
+// plain write-back st.global: in an L2 gather stream with one 512-B store per 8 gathers, .cs
+// stores cost ~6% of the gather rate (tools/microbench/mb11.cu, profiles/r02).
+template <int kB>
+__device__ __forceinline__ void band_batch(uint4 &acc, const uint32_t (&f)[kB], const uint4 (&v)[kB], uint8_t *&out,
+                                           uint32_t t, bool active, uint32_t lane) {
+  uint32_t sel = 0;
+#pragma unroll
+  for (int u = 0; u < kB; ++u) sel = lane == static_cast<uint32_t>(u) ? f[u] : sel;
+  const uint32_t ends = __ballot_sync(0xffffffffu, lane < static_cast<uint32_t>(kB) && static_cast<int32_t>(sel) < 0);
+  if (ends == 0u) {
+#pragma unroll
+    for (int u = 0; u + 1 < kB; u += 2) {
+      acc.x ^= v[u].x ^ v[u + 1].x;
+      acc.y ^= v[u].y ^ v[u + 1].y;
+      acc.z ^= v[u].z ^ v[u + 1].z;
+      acc.w ^= v[u].w ^ v[u + 1].w;
+    }
+    if (kB & 1) xor_into(acc, v[kB - 1]);
+  } else {
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      xor_into(acc, v[u]);
+      if (ends & (1u << u)) {
+        if (active) *reinterpret_cast<uint4 *>(out) = acc;
+        out += t;
+        acc = make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+}
+
+constexpr int kBand4Threads = 64;  // 2-warp blocks: a block slot frees as soon as its 2 warps finish
+template <int kB, int kMinBlocks, int kBT = kGlobalThreads>
+__global__ void __launch_bounds__(kBT, kMinBlocks)
+    fsb_lt_band4(uint32_t S, uint32_t k, uint32_t t, uint32_t col0, uint32_t col1, uint32_t nbands, uint32_t row_begin,
+                 uint32_t nrows, uint32_t band_rows, const int32_t *__restrict__ row_ptr,
+                 const uint32_t *__restrict__ colf, const uint8_t *__restrict__ data, uint64_t data_stride,
+                 const uint8_t *__restrict__ checks, uint64_t checks_stride, uint8_t *__restrict__ coded,
+                 uint64_t coded_stride) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the precode launch (PDL)
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nchunks = (nrows + band_rows - 1) / band_rows;
+  const uint32_t unit = blockIdx.x * (kBT / 32) + (threadIdx.x >> 5);  // < 2^31 (host check)
+  const uint32_t chunk = unit % nchunks;
+  const uint32_t rest = unit / nchunks;
+  const uint32_t band = rest % nbands;
+  const uint32_t s = rest / nbands;
+  if (s >= S) return;
+  const uint32_t byte_raw = col0 + band * kBandBytes + lane * 16;
+  const bool active = byte_raw < col1;
+  const uint32_t byte = active ? byte_raw : col0;
+  const uint8_t *dbase = data + s * data_stride + byte;
+  const uint8_t *cbase = checks + s * checks_stride + byte - static_cast<uint64_t>(k) * t;
+  const uint32_t r0 = chunk * band_rows;
+  const uint32_t rows = min(band_rows, nrows - r0);
+  const int32_t base = __ldg(&row_ptr[row_begin + r0]);
+  const int32_t end = __ldg(&row_ptr[row_begin + r0 + rows]);
+  uint8_t *out = coded + s * coded_stride + static_cast<uint64_t>(r0) * t + byte_raw;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  const int32_t head = (end - base) % kB;  // the partial batch, first
+  int32_t e0 = base;
+  uint32_t cv = static_cast<int32_t>(lane) < end - base ? __ldg(&colf[base + lane]) : 0u;
+  int32_t kk = 0;
+  if (head) {
+    uint32_t f[kB];
+    uint4 v[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      f[u] = __shfl_sync(0xffffffffu, cv, u);
+      if (u >= head) f[u] = 0;
+      v[u] = make_uint4(0, 0, 0, 0);
+      if (u < head) v[u] = ldg16(src_addr(f[u], k, t, dbase, cbase));
+    }
+    band_batch<kB>(acc, f, v, out, t, active, lane);
+    kk = head;
+  }
+  while (e0 < end) {  // windows of up to 32 indices; after the head every batch is full
+    const int32_t nb = min(32, end - e0);
+    for (; kk + kB <= nb; kk += kB) {
+      uint32_t f[kB];
+      uint4 v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        f[u] = __shfl_sync(0xffffffffu, cv, (kk + u) & 31);
+        v[u] = ldg16(src_addr(f[u], k, t, dbase, cbase));
+      }
+      band_batch<kB>(acc, f, v, out, t, active, lane);
+    }
+    e0 += kk;
+    kk = 0;
+    cv = static_cast<int32_t>(lane) < end - e0 ? __ldg(&colf[e0 + lane]) : 0u;
   }
 }
 
@@ -1048,21 +1164,30 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     const uint64_t units = static_cast<uint64_t>(S) * nbands * ((nrows + band_rows - 1) / band_rows);
     const uint64_t blocks = (units + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
     if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
-    // (gathers in flight per warp, blocks per SM); measured on config 5 (tools/gpu/sweep_band.sh):
-    // (2, 8) 0.281 ms, (4, 6) 0.292, (8, 4) 0.299, (8, 5) 0.371 (spills), (4, 8) 0.381 (spills).
-    // Tuning knob FSB_BAND_CFG selects another instance.
+    // Many-wave calls (config 5: 13 waves) take fsb_lt_band4: 4 gathers per batch, 2-warp blocks,
+    // 48 warps per SM (same-box A/B, tools/gpu/ab/run_multi.sh, profiles/r02: 0.252 ms vs 0.278
+    // for fsb_lt_band<2, 8> with 8-warp blocks; 2-warp blocks alone 0.263 -> 0.252).  Calls of
+    // only a few waves end on their heaviest rows' serial gather chains and keep the lazily
+    // waiting fsb_lt_band<4, 6> (config 3: 35.2 -> 30.1 us vs 2 in flight).  FSB_BAND_CFG: 4 =
+    // this rule (default), 1 = fsb_lt_band<2, 8> for many-wave calls (round-1 kernel), 0 = always
+    // <4, 6>, 2 = <8, 4>.
     static const int band_cfg = [] {
       const char *e = std::getenv("FSB_BAND_CFG");
       return e ? std::atoi(e) : 4;
     }();
-    // A call of only a few waves of warps ends on its heaviest rows' serial gather chains; there 4
-    // gathers in flight beat 2 (config 3: 35.2 -> 30.1 us; config 5, 13 waves, keeps (2, 8)).
     const bool few_waves = units < 4ull * g.sm_count * 64;
     auto kern = (band_cfg == 0 || (band_cfg == 4 && few_waves)) ? fsb_lt_band<4, 6, true> : fsb_lt_band<2, 8, false>;
     if (band_cfg == 2) kern = fsb_lt_band<8, 4, false>;
+    uint64_t blocks_launch = blocks;
+    uint32_t block_threads = kGlobalThreads;
+    if (band_cfg == 4 && !few_waves) {
+      kern = fsb_lt_band4<4, 24, kBand4Threads>;
+      block_threads = kBand4Threads;
+      blocks_launch = (units + kBand4Threads / 32 - 1) / (kBand4Threads / 32);
+    }
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(static_cast<uint32_t>(blocks));
-    lc.blockDim = dim3(kGlobalThreads);
+    lc.gridDim = dim3(static_cast<uint32_t>(blocks_launch));
+    lc.blockDim = dim3(block_threads);
     lc.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -65,23 +65,27 @@ def _worker(rank, ws, port, cid, mode, q):
                 cod = torch.full((n, t), 0x5A, dtype=torch.uint8, device="cuda")
                 g.encode_range(d, chk, cod, 0, n, c0, c1)
                 torch.cuda.synchronize()
-                blk = cod[:, c0:c1].contiguous().cpu()
+                # this rank's column block of coded rows and checks (rows first, then checks)
+                blk = torch.cat([cod[:, c0:c1], chk[:, c0:c1]]).contiguous().cpu()
                 untouched = bool((cod[:, :c0] == 0x5A).all() and (cod[:, c1:] == 0x5A).all())
                 parts = [None] * ws
                 dist.all_gather_object(parts, (c0, c1, untouched))
                 if rank == 0:
-                    Y = torch.empty((n, t), dtype=torch.uint8)
-                    Y[:, c0:c1] = blk
+                    full = torch.empty((n + p, t), dtype=torch.uint8)
+                    full[:, c0:c1] = blk
                     for r in range(1, ws):
                         r0, r1, _ = parts[r]
-                        tmp = torch.empty((n, r1 - r0), dtype=torch.uint8)
+                        tmp = torch.empty((n + p, r1 - r0), dtype=torch.uint8)
                         dist.recv(tmp, r)
-                        Y[:, r0:r1] = tmp
+                        full[:, r0:r1] = tmp
                     assert all(u for _, _, u in parts), "bytes outside a rank's columns were written"
+                    Y, chk_all = full[:n], full[n:]
                 else:
                     dist.send(blk, 0)
                     Y = None
-            C = chk.cpu()[None] if rank == 0 else None
+            if mode == "rows":
+                chk_all = chk.cpu()                            # every rank computes all p checks
+            C = chk_all[None] if rank == 0 else None
             if Y is not None:
                 Y = Y[None]
         dist.barrier()

@@ -531,3 +531,37 @@ def test_encode_host_ragged_sizes(t, S, p, chunks):
     _assert_equal(h_y.numpy(), Y, "coded")
     if p:
         _assert_equal(h_c.numpy(), C, "checks")
+
+
+@pytest.mark.parametrize("seed,t,S,dist", [(11, 1008, 160, "omega"), (12, 2064, 96, "rsd"), (13, 528, 300, "omega")])
+def test_many_wave_band_kernel_ragged(seed, t, S, dist):
+    """fsb_lt_band4 (the GLOBAL band kernel for calls of many waves of warps): a random code with
+    a ragged last band (t not a multiple of 512), many stripes, degree-1 rows and a heavy tail;
+    every stripe in full against the oracle, plus a row-range partition of one stripe."""
+    _need_gpu()
+    rng = np.random.default_rng(seed)
+    k = int(rng.integers(300, 900))
+    p = int(rng.integers(1, 20))
+    cfg = dict(name="mw", k=k, p=p, d_p=3, n=int(1.3 * (k + p)), t=t, stripes=S, seed=seed)
+    if dist == "omega":
+        cfg.update(dist=configs.FINITE, fin_deg=configs.OMEGA_DEGREES, fin_prob=configs.OMEGA_PROBS)
+    else:
+        cfg.update(dist=configs.RSD, rsd_c=0.1, rsd_delta=0.05)
+    g = fsb.Graph.create(cfg)
+    g.set_variant(fsb.VARIANT_GLOBAL)
+    go = oracle.generate_graph(cfg)
+    D = inputs.stripe_data(cfg).numpy()
+    C, Y = oracle.encode(go, D)
+    d = torch.from_numpy(D).cuda()
+    chk = torch.empty((S, p, t), dtype=torch.uint8, device="cuda")
+    cod = torch.empty((S, cfg["n"], t), dtype=torch.uint8, device="cuda")
+    g.encode_stripes(d, chk, cod)
+    torch.cuda.synchronize()
+    assert fsb.last_launch_count() == 2
+    _assert_equal(chk.cpu().numpy(), C, "checks")
+    _assert_equal(cod.cpu().numpy(), Y, "coded")
+    a, b = cfg["n"] // 5, cfg["n"] - 3
+    out = torch.empty((b - a, t), dtype=torch.uint8, device="cuda")
+    g.encode(d[1], chk[1], out, a, b)
+    torch.cuda.synchronize()
+    _assert_equal(out.cpu().numpy(), Y[1][a:b], "row range")
