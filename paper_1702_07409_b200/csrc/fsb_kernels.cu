@@ -269,7 +269,9 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
   }
 }
 
-// Tile i of this CTA: (stripe, slice).  Unpaired: tile blockIdx.x + i*gridDim.x of S x nslices.
+// Tile i of this CTA: (stripe, slice).  (Recomputed with two divisions per tile on purpose: an
+// incremental iterator kept ~8 more registers live across the consumers' item loop and made
+// config 4 6% slower, 0.597 -> 0.631 ms, profiles/r02/ab_r02o.txt.)  Unpaired: tile blockIdx.x + i*gridDim.x of S x nslices.
 // Paired: pair blockIdx.x + (i/2)*gridDim.x of S x nslices/2, slice 2*(pair % (nslices/2)) plus
 // (i&1), flipped on odd CTAs: half the SMs write their lines while the other half park, so the
 // HBM write stream stays even instead of pulsing with the tile pairs.
