@@ -383,7 +383,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t i = 1; tile_of(a, i, stripe, slice); ++i) {  // tile 0: issued above
         const uint32_t b = i & 1, ph = (i >> 1) & 1;
         const uint32_t buf = smem_base + b * buf_bytes;
+        const long long tw0 = (a.debug & 2) ? clock64() : 0;
         mbar_wait(smem_u32(&empty[b]), ph ^ 1);  // consumers released tile i-2
+        if (a.debug & 2) atomicAdd(&g_debug_counters[60], static_cast<unsigned long long>(clock64() - tw0));
         if (a.debug & 1) {  // experiment: no TMA (consumers gather stale rows)
           mbar_arrive(smem_u32(&full[b]));
         } else {
@@ -404,10 +406,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t pw = warp - kConsumerWarps - 1;                  // precode warp 0..kPrecodeWarps-1
     const uint32_t half_id = pw * kHalvesPerWarp + (lane >> 2), lane4 = lane & 3;
     uint32_t stripe, slice;
+    const long long pt0 = (a.debug & 2) ? clock64() : 0;
     for (uint32_t i = 0; tile_of(a, i, stripe, slice); ++i) {
       const uint32_t b = i & 1, ph = (i >> 1) & 1;
       const uint32_t buf = smem_base + b * buf_bytes;
+      const long long tw0 = (a.debug & 2) ? clock64() : 0;
       mbar_wait(smem_u32(&full[b]), ph);
+      if ((a.debug & 2) && lane == 0)
+        atomicAdd(&g_debug_counters[48 + 2 * pw], static_cast<unsigned long long>(clock64() - tw0));
       // precode, level by level (a check may read checks of earlier levels, Alg 2): check c of
       // a level by half-group (c - level start) % 8, 16 B per lane
       const uint32_t lb = buf + lane4 * 16;
@@ -437,6 +443,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (pw == 0 && lane == 0) mbar_arrive(smem_u32(&ready[b]));  // release: data + checks visible
     }
+    if ((a.debug & 2) && lane == 0)
+      atomicAdd(&g_debug_counters[49 + 2 * pw], static_cast<unsigned long long>(clock64() - pt0));
     return;
   }
 
