@@ -148,9 +148,6 @@ typedef struct {
   uint32_t sched_steps_max;  /* SMEM schedule: gather slots of the most loaded warp per tile  */
   uint32_t sched_steps_avg;  /* SMEM schedule: mean gather slots per warp per tile (rounded)  */
   int32_t device;            /* CUDA device of the device copy, -1 for host-only graphs       */
-  uint32_t tmem_quarter_max; /* SMEM schedule: TMEM columns the fullest lane quarter needs to
-                                park paired-tile halves and hold the schedule (<= 512: the
-                                paired tiles run in TMEM-schedule mode, fsb_smem_encode<true>) */
 } fs_graph_info;
 
 FSB_API fs_status fs_graph_get_info(const fs_graph *g, fs_graph_info *info);

@@ -536,51 +536,6 @@ void build_smem_schedule(Graph &g) {
     per_warp[l.second].push_back(idx);
     heap.push({l.first + cost(items[idx]), l.second});
   }
-  // Warp lists -> warp slots, balancing the TMEM columns of the four lane quarters (warp w uses
-  // quarter w % 4): a list needs 4 columns per item to park its rows' halves and 4 per schedule
-  // chunk (heads + continuations) in TMEM-schedule mode.  Swapping whole lists between warps
-  // keeps the LPT balance of the warps' work.
-  {
-    auto ncont = [](const Item &it) {
-      return it.len > kHeadSlots ? (it.len - kHeadSlots + kChunkSlots - 1) / kChunkSlots : 0u;
-    };
-    std::vector<uint32_t> use(kConsumerWarps, 0), items_w(kConsumerWarps, 0), conts_w(kConsumerWarps, 0);
-    for (int w = 0; w < kConsumerWarps; ++w) {
-      for (uint32_t idx : per_warp[w]) conts_w[w] += ncont(items[idx]);
-      items_w[w] = static_cast<uint32_t>(per_warp[w].size());
-      use[w] = 4 * (2 * items_w[w] + conts_w[w]);
-    }
-    std::vector<int> ord(kConsumerWarps);
-    std::iota(ord.begin(), ord.end(), 0);
-    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return use[a] > use[b]; });
-    uint32_t qsum[4] = {0, 0, 0, 0}, qcnt[4] = {0, 0, 0, 0};
-    std::vector<std::vector<uint32_t>> placed(kConsumerWarps);
-    std::vector<int> src_of(kConsumerWarps, -1);
-    for (int w : ord) {
-      int best = -1;
-      for (int q = 0; q < 4; ++q)
-        if (qcnt[q] < kConsumerWarps / 4 && (best < 0 || qsum[q] < qsum[best])) best = q;
-      const int slot = best + 4 * static_cast<int>(qcnt[best]++);
-      qsum[best] += use[w];
-      placed[slot] = std::move(per_warp[w]);
-      src_of[slot] = w;
-    }
-    per_warp = std::move(placed);
-    s.tmem_quarter_max = std::max(std::max(qsum[0], qsum[1]), std::max(qsum[2], qsum[3]));
-    s.tmem_sched = s.tmem_quarter_max <= 512;
-    s.warp_tcols.assign(kConsumerWarps, 0);
-    s.chunks_w.assign(kConsumerWarps, 0);
-    uint32_t park[4] = {0, 0, 0, 0}, sched[4] = {0, 0, 0, 0};
-    for (int w = 0; w < kConsumerWarps; ++w) park[w & 3] += 4 * items_w[src_of[w]];
-    for (int q = 0; q < 4; ++q) sched[q] = park[q], park[q] = 0;   // schedules after the quarter's parking
-    for (int w = 0; w < kConsumerWarps; ++w) {
-      const int src = src_of[w];
-      s.chunks_w[w] = items_w[src] + conts_w[src];
-      s.warp_tcols[w] = park[w & 3] | sched[w & 3] << 16;
-      park[w & 3] += 4 * items_w[src];
-      sched[w & 3] += 4 * s.chunks_w[w];
-    }
-  }
 #ifdef FSB_EXPERIMENTS
   // profiling experiment (FSB_SCHED_DEBUG=zero): every slot reads a zero row of its half's parity
   // -- output is wrong by design, so it exists only in experiment builds (-DFSB_EXPERIMENTS)

@@ -74,13 +74,6 @@ struct SmemSchedule {
   uint32_t data_units = 0, tile_units = 0;
   uint32_t steps_max = 0, steps_total = 0;  // gather slots per half-group per warp: max, sum
   uint32_t pad_slots = 0;               // slots that read a zero row (parity / length padding)
-  // TMEM-schedule mode of paired tiles (fsb_smem_encode<true>): every consumer warp's parked
-  // halves (4 columns per item) and schedule chunks (4 columns per chunk, heads then
-  // continuations) in its lane quarter; usable when every quarter needs <= 512 columns
-  bool tmem_sched = false;
-  uint32_t tmem_quarter_max = 0;        // columns the fullest lane quarter needs
-  std::vector<uint32_t> warp_tcols;     // per warp: park column | schedule column << 16
-  std::vector<uint32_t> chunks_w;       // per warp: heads + continuation chunks
 };
 
 struct DeviceBufs {

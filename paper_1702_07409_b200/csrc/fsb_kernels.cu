@@ -36,10 +36,6 @@
 #include "fsb_internal.h"
 
 
-#ifndef FSB_TS_SMEM_SCHED
-#define FSB_TS_SMEM_SCHED 0  // A/B: TMEM-schedule mode's layout and stores, chunks from shared memory
-#endif
-
 namespace fsb {
 
 // --------------------------------------------------------------------------- PTX helpers
@@ -92,31 +88,6 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int32_t c0,
-                                            int32_t c1, int32_t c2, int32_t c3, int32_t c4) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
-      : "memory");
-}
-// The tile's data rows: unit u (kUnitRows rows) of (stripe, 64-B slice).  TMEM-schedule mode: the
-// slice is the EVEN (slice & 1 == 0) or ODD 16-B pieces of 128-B column slice >> 1 (5-D map
-// {16 B, half, 32-B piece pair, row, stripe}); otherwise 64 contiguous bytes (3-D map).
-template <bool kTS>
-__device__ __forceinline__ void tma_tile_unit(uint32_t dst, const CUtensorMap *map, uint32_t bar, uint32_t slice,
-                                              uint32_t u, uint32_t stripe) {
-#if defined(FSB_EXPERIMENTS) && defined(FSB_TS_TMA3D)
-  if constexpr (false)  // experiment: contiguous 64-B slices in TMEM-schedule mode (wrong bytes by design)
-#else
-  if constexpr (kTS)
-#endif
-    tma_load_5d(dst, map, bar, 0, static_cast<int32_t>(slice & 1), static_cast<int32_t>((slice >> 1) * 4),
-                static_cast<int32_t>(u * kUnitRows), static_cast<int32_t>(stripe));
-  else
-    tma_load_3d(dst, map, bar, static_cast<int32_t>(slice * kSliceBytes), static_cast<int32_t>(u * kUnitRows),
-                static_cast<int32_t>(stripe));
-}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -150,31 +121,6 @@ __device__ __forceinline__ uint4 tmem_ld16(uint32_t taddr) {
   return v;
 }
 
-// Asynchronous 16-B TMEM load (no wait): the registers are defined only after tmem_wait(v).
-__device__ __forceinline__ uint4 tmem_ld16_async(uint32_t taddr) {
-  uint4 v;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "r"(taddr)
-               : "memory");
-  return v;
-}
-// Wait for this thread's outstanding tcgen05.ld; v is an operand so no use of it can be
-// scheduled above the wait.
-__device__ __forceinline__ void tmem_wait(uint4 &v) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)::"memory");
-}
-__device__ __forceinline__ void tmem_wait2(uint4 &v, uint4 &w) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w), "+r"(w.x), "+r"(w.y), "+r"(w.z), "+r"(w.w)::"memory");
-}
-// 32 contiguous bytes per lane: a half-group's 4 lanes write one full 128-B line.
-__device__ __forceinline__ void st_stream32(uint8_t *p, const uint4 &a, const uint4 &b) {
-  asm volatile("st.global.cs.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
-               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
-               : "memory");
-}
-
 // ============================================================================ SMEM kernel
 // Profiling experiments only (FSB_DEBUG=2): per consumer warp, cycles spent waiting for a tile
 // (ready/full barriers) and total cycles, summed over CTAs (read with fs_debug_counters).
@@ -197,10 +143,6 @@ struct SmemArgs {
   uint32_t tmem_cols;          // TMEM columns allocated per CTA in paired mode (power of 2)
   uint32_t debug;              // FSB_DEBUG bits (profiling experiments only; 0 in production)
   uint32_t wait_ns;            // consumer sleep between probes of a tile's `ready` barrier
-  // TMEM-schedule mode (fsb_smem_encode<true>): per consumer warp, the TMEM column of its parked
-  // halves (low 16 bits) and of its schedule chunks (high 16 bits), in its lane quarter
-  uint32_t warp_tcols[kConsumerWarps];
-  uint32_t sched_chunks_w[kConsumerWarps];  // chunks (heads + conts) of each warp
 };
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -327,88 +269,9 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
   }
 }
 
-// One item of the TMEM-schedule mode (fsb_smem_encode<true>, paired tiles only).  The pair's two
-// tiles hold the EVEN and the ODD 16-B pieces of a 128-B column (a 5-D TMA box with a 32-B piece
-// stride), so lane j of half-group h computes bytes [32j, 32j+16) of its row in one tile and
-// [32j+16, 32j+32) in the other: after the second tile the lane owns 32 contiguous bytes and the
-// half-group writes the row's full 128-B line with one 256-bit store per lane -- each half-group
-// reads only its own schedule (no partner swap).  Schedule chunks come from TMEM (tcgen05.ld),
-// off the shared-memory pipe the gathers saturate.  kMode 1 parks, 2 stores; `lo_first` = the
-// parked tile holds the even pieces.
-__device__ __forceinline__ void lt_item_ts(const uint4 &h, uint32_t &ccol, uint32_t sbase, uint8_t *out, uint64_t t,
-                                           uint32_t half_id, uint32_t tcol, int kMode, bool lo_first) {
-  const uint32_t row = h.x & 0xFFFFu;
-  const uint32_t ctrl = h.x >> 16;
-  const uint32_t L = ctrl & kMaxItemLen;
-  uint4 acc = make_uint4(0, 0, 0, 0);
-  uint4 c = make_uint4(0, 0, 0, 0);
-#if FSB_TS_SMEM_SCHED
-  // A/B: chunks from the shared-memory copy (ccol = shared address of this half-group's chunk)
-  if (L > kHeadSlots) c = lds128(ccol);
-  gather_xor_n<2>(acc, h, L < kHeadSlots ? L : kHeadSlots, sbase);
-  if (L > kHeadSlots) {
-    uint32_t rem = L - kHeadSlots;
-    ccol += kChunkBytes;
-    for (; rem > kChunkSlots; rem -= kChunkSlots) {
-      const uint4 nx = lds128(ccol);
-      ccol += kChunkBytes;
-      gather_xor<0, 8>(acc, c, sbase);
-      c = nx;
-    }
-    gather_xor_n<0>(acc, c, rem, sbase);
-  }
-#else
-  if (L > kHeadSlots) c = tmem_ld16_async(ccol);
-  gather_xor_n<2>(acc, h, L < kHeadSlots ? L : kHeadSlots, sbase);
-  if (L > kHeadSlots) {
-    tmem_wait(c);
-    uint32_t rem = L - kHeadSlots;
-    ccol += 4;
-    for (; rem > kChunkSlots; rem -= kChunkSlots) {
-      uint4 nx = tmem_ld16_async(ccol);  // next chunk in flight while this one is gathered
-      ccol += 4;
-      gather_xor<0, 8>(acc, c, sbase);
-      tmem_wait(nx);
-      c = nx;
-    }
-    gather_xor_n<0>(acc, c, rem, sbase);
-  }
-#endif
-  const bool wsplit = ctrl & kSplitBit;
-  if (wsplit) {
-#pragma unroll
-    for (int o = 4; o <= 16; o <<= 1) {
-      acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, o);
-      acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, o);
-      acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, o);
-      acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, o);
-    }
-  } else if (ctrl & kPairSplitBit) {
-    uint4 o;
-    o.x = __shfl_xor_sync(0xffffffffu, acc.x, 4);
-    o.y = __shfl_xor_sync(0xffffffffu, acc.y, 4);
-    o.z = __shfl_xor_sync(0xffffffffu, acc.z, 4);
-    o.w = __shfl_xor_sync(0xffffffffu, acc.w, 4);
-    if (h.y & kPairFlag) xor_into(acc, o);
-  }
-  if (kMode == 1) {
-    tmem_st16(tcol, acc);
-  } else {
-    uint4 prev = tmem_ld16_async(tcol);
-    tmem_wait(prev);
-    const bool st = wsplit ? half_id == 0 : row != kNoRow;
-    if (st) {
-      uint8_t *dst = out + static_cast<uint64_t>(row) * t;
-      if (lo_first) st_stream32(dst, prev, acc);
-      else st_stream32(dst, acc, prev);
-    }
-  }
-}
-
-// Tile i of this CTA: (stripe, slice).  Unpaired: tile blockIdx.x + i*gridDim.x of S x nslices.
-// (Recomputed with two divisions per tile on purpose: an incremental iterator kept ~8 more
-// registers live across the consumers' item loop and made config 4 6% slower, 0.597 -> 0.631 ms,
-// profiles/r02/ab_r02o.txt.)
+// Tile i of this CTA: (stripe, slice).  (Recomputed with two divisions per tile on purpose: an
+// incremental iterator kept ~8 more registers live across the consumers' item loop and made
+// config 4 6% slower, 0.597 -> 0.631 ms, profiles/r02/ab_r02o.txt.)  Unpaired: tile blockIdx.x + i*gridDim.x of S x nslices.
 // Paired: pair blockIdx.x + (i/2)*gridDim.x of S x nslices/2, slice 2*(pair % (nslices/2)) plus
 // (i&1), flipped on odd CTAs: half the SMs write their lines while the other half park, so the
 // HBM write stream stays even instead of pulsing with the tile pairs.
@@ -439,7 +302,6 @@ __device__ __forceinline__ bool tile_of(const SmemArgs &a, uint32_t i, uint32_t 
 //     TMEM-parked halves and full 128-B lines paired).
 // Buffers alternate (tile i uses buffer i&1), so tile i+1 streams in while tile i computes, and a
 // consumer warp that finishes tile i early starts tile i+1 without waiting for the others.
-template <bool kTS>
 __global__ void __launch_bounds__(kThreads, 1)
     fsb_smem_encode(const __grid_constant__ CUtensorMap tmap, const SmemArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -479,13 +341,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         mbar_arrive_expect_tx(smem_u32(&full[0]), a.data_units * kUnitBytes);
         for (uint32_t u = 0; u < a.data_units; ++u)
-          tma_tile_unit<kTS>(smem_base + u * kUnitBytes, &tmap, smem_u32(&full[0]), slice, u, stripe);
+          tma_load_3d(smem_base + u * kUnitBytes, &tmap, smem_u32(&full[0]), static_cast<int32_t>(slice * kSliceBytes),
+                      static_cast<int32_t>(u * kUnitRows), static_cast<int32_t>(stripe));
       }
     }
   }
-  // the schedule (identical for every tile; TMEM-schedule mode: each consumer warp copies its own
-  // chunks into TMEM below) and the two zero rows of each buffer
-  if (!kTS || FSB_TS_SMEM_SCHED) {  // 4 loads in flight per thread, then their stores (the copy is on every launch's critical path)
+  // the schedule (identical for every tile) and the two zero rows of each buffer
+  {  // 4 loads in flight per thread, then their stores (the copy is on every launch's critical path)
     const uint32_t nx = a.sched_chunks * (kChunkBytes / 16);
     for (uint32_t x0 = threadIdx.x; x0 < nx; x0 += 4 * blockDim.x) {
       uint4 v[4];
@@ -530,7 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive_expect_tx(smem_u32(&full[b]), a.data_units * kUnitBytes);
         }
         for (uint32_t u = 0; u < a.data_units && !(a.debug & 1); ++u)
-          tma_tile_unit<kTS>(buf + u * kUnitBytes, &tmap, smem_u32(&full[b]), slice, u, stripe);
+          tma_load_3d(buf + u * kUnitBytes, &tmap, smem_u32(&full[b]), static_cast<int32_t>(slice * kSliceBytes),
+                      static_cast<int32_t>(u * kUnitRows), static_cast<int32_t>(stripe));
       }
     }
     return;
@@ -554,10 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // precode, level by level (a check may read checks of earlier levels, Alg 2): check c of
       // a level by half-group (c - level start) % 8, 16 B per lane
       const uint32_t lb = buf + lane4 * 16;
-      // this lane's 16 B of the slice in the row: contiguous (64 B per slice), or in TMEM-schedule
-      // mode 16-B piece lane4 of the even / odd pieces of 128-B column slice >> 1
-      const uint64_t col_off = kTS ? static_cast<uint64_t>(slice >> 1) * 128 + lane4 * 32 + (slice & 1) * 16
-                                   : static_cast<uint64_t>(slice) * kSliceBytes + lane4 * 16;
+      const uint64_t col_off = static_cast<uint64_t>(slice) * kSliceBytes + lane4 * 16;
       for (uint32_t L = 0; L < a.pre_levels; ++L) {
         const uint32_t c0 = __ldg(&a.pre_level_ptr[L]), c1 = __ldg(&a.pre_level_ptr[L + 1]);
         for (uint32_t c = c0 + half_id; c < c1; c += kHalvesPerWarp * kPrecodeWarps) {
@@ -591,74 +451,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ------------------------------------------------------------------- consumer warps
   const uint32_t half_id = lane >> 2, lane4 = lane & 3;
   const uint32_t nitems = __ldg(&a.warp_info[warp * 3 + 0]);
-  if constexpr (kTS) {
-    // TMEM-schedule mode (paired tiles): this warp's chunks -- heads, then continuations -- into
-    // its schedule columns once per launch; every tile then reads them with tcgen05.ld
-    const uint32_t tq = *tmem_slot + ((32u * (warp & 3)) << 16);
-    const uint32_t tpark = tq + (a.warp_tcols[warp] & 0xFFFFu), tsched = tq + (a.warp_tcols[warp] >> 16);
-    const uint32_t nch = a.sched_chunks_w[warp];
-    const uint32_t hoff = __ldg(&a.warp_info[warp * 3 + 1]), coff = a.cont_base + __ldg(&a.warp_info[warp * 3 + 2]);
-    for (uint32_t c = 0; c < nch; ++c) {
-      const uint32_t chunk = c < nitems ? hoff + c : coff + (c - nitems);
-      tmem_st16(tsched + 4 * c, __ldg(a.sched + chunk * (kChunkBytes / 16) + half_id));
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    const uint32_t tlast = tsched + 4 * (nitems ? nitems - 1 : 0);  // prefetch clamp
-    const bool lo_first = (blockIdx.x & 1) == 0;  // the parked (first) tile of a pair = even pieces
-    const long long t_start = (a.debug & 2) ? clock64() : 0;
-    uint32_t stripe, slice;
-    for (uint32_t i = 0; tile_of(a, i, stripe, slice); ++i) {
-      const uint32_t b = i & 1, ph = (i >> 1) & 1;
-      const int mode = 1 + (i & 1);
-      const uint32_t sbase = smem_base + b * buf_bytes + lane4 * 16;
-#if FSB_TS_SMEM_SCHED
-      uint32_t ccol = smem_u32(sched_s) + (a.cont_base + __ldg(&a.warp_info[warp * 3 + 2])) * kChunkBytes + half_id * 16;
-      const uint32_t hb = smem_u32(sched_s) + __ldg(&a.warp_info[warp * 3 + 1]) * kChunkBytes + half_id * 16;
-      uint4 h0 = lds128(hb);
-#else
-      uint32_t ccol = tsched + 4 * nitems;
-      uint4 h0 = tmem_ld16_async(tsched);
-#endif
-      long long t_wait0 = 0;
-      if (a.debug & 2) t_wait0 = clock64();
-      if (a.wait_ns) mbar_wait_backoff(smem_u32(&ready[b]), ph, a.wait_ns);
-      else mbar_wait(smem_u32(&ready[b]), ph);
-      mbar_wait(smem_u32(&full[b]), ph);
-      if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2], static_cast<unsigned long long>(clock64() - t_wait0));
-      uint8_t *out = a.coded + stripe * a.coded_stride + static_cast<uint64_t>(slice >> 1) * 128 + lane4 * 32;
-#if FSB_TS_SMEM_SCHED
-      for (uint32_t it = 0; it < nitems; it += 2) {
-        const uint4 h1 = lds128(hb + (it + 1) * kChunkBytes);
-        lt_item_ts(h0, ccol, sbase, out, a.t, half_id, tpark + 4 * it, mode, lo_first);
-        if (it + 1 >= nitems) break;
-        h0 = lds128(hb + (it + 2) * kChunkBytes);
-        lt_item_ts(h1, ccol, sbase, out, a.t, half_id, tpark + 4 * (it + 1), mode, lo_first);
-      }
-#else
-      tmem_wait(h0);
-      for (uint32_t it = 0; it < nitems; it += 2) {
-        uint4 h1 = tmem_ld16_async(min(tsched + 4 * (it + 1), tlast));
-        lt_item_ts(h0, ccol, sbase, out, a.t, half_id, tpark + 4 * it, mode, lo_first);
-        tmem_wait(h1);
-        if (it + 1 >= nitems) break;
-        h0 = tmem_ld16_async(min(tsched + 4 * (it + 2), tlast));
-        lt_item_ts(h1, ccol, sbase, out, a.t, half_id, tpark + 4 * (it + 1), mode, lo_first);
-        tmem_wait(h0);
-      }
-#endif
-      if (mode == 1) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // parked before reuse
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&empty[b]));
-    }
-    if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2 + 1], static_cast<unsigned long long>(clock64() - t_start));
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    consumer_bar();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 0)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(a.tmem_cols)
-                   : "memory");
-    return;
-  }
   const uint32_t head_b = smem_u32(sched_s) + __ldg(&a.warp_info[warp * 3 + 1]) * kChunkBytes;
   const uint32_t cont_b = smem_u32(sched_s) + (a.cont_base + __ldg(&a.warp_info[warp * 3 + 2])) * kChunkBytes;
   // TMEM: this warp's lane quarter (warp % 4) and its column block after the earlier warps of the
@@ -1191,11 +983,8 @@ fs_status upload_graph(Graph &g) {
       if ((st = upload(&g.dev.warp_info, g.sched.warp_info.data(), g.sched.warp_info.size())) != FS_OK) return st;
       if ((st = upload(&g.dev.pre_slots, g.sched.pre_slots.data(), g.sched.pre_slots.size())) != FS_OK) return st;
       if ((st = upload(&g.dev.pre_level_ptr, g.pre_level_ptr.data(), g.pre_level_ptr.size())) != FS_OK) return st;
-      e = cudaFuncSetAttribute(fsb_smem_encode<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(fsb_smem_encode, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(g.smem_bytes));
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(fsb_smem_encode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(g.smem_bytes));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     }
   }
@@ -1344,38 +1133,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = attr;
     lc.numAttrs = pdl_enabled() ? 1 : 0;  // the prologue may overlap the previous grid's tail
-    // TMEM-schedule mode for paired tiles whose schedule fits TMEM (FSB_TMEM_SCHED=0 disables)
-    static const int tmem_sched_env = [] {
-      const char *e = std::getenv("FSB_TMEM_SCHED");
-      return e ? std::atoi(e) : 1;
-    }();
-    const bool ts = a.paired && g.sched.tmem_sched && tmem_sched_env && prm.t % 128 == 0;
-    if (ts) {
-      // 5-D view {16 B, half, 32-B piece pair, row, stripe}: a box {16, 1, 4, 64, 1} lands the even
-      // (half 0) or odd (half 1) 16-B pieces of a 128-B column as 64-B shared-memory rows
-      const cuuint64_t dims5[5] = {16, 2, prm.t / 32, prm.k, S};
-      const cuuint64_t strides5[4] = {16, 32, prm.t, data_stride};
-      const cuuint32_t box5[5] = {16, 1, 4, kUnitRows, 1};
-      const cuuint32_t estr5[5] = {1, 1, 1, 1, 1};
-#if defined(FSB_EXPERIMENTS) && defined(FSB_TS_TMA3D)
-      CUresult r5 = CUDA_SUCCESS;  // experiment: keep the 3-D map
-      (void)dims5, (void)strides5, (void)box5, (void)estr5;
-#else
-      CUresult r5 = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t *>(data), dims5, strides5,
-                           box5, estr5, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-#endif
-      if (r5 != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled (5-D) failed (code " + std::to_string(static_cast<int>(r5)) + ")");
-        return FS_ECUDA;
-      }
-      a.tmem_cols = 512;
-      for (int w = 0; w < kConsumerWarps; ++w) {
-        a.warp_tcols[w] = g.sched.warp_tcols[w];
-        a.sched_chunks_w[w] = g.sched.chunks_w[w];
-      }
-    }
-    e = ts ? cudaLaunchKernelEx(&lc, fsb_smem_encode<true>, tmap, a) : cudaLaunchKernelEx(&lc, fsb_smem_encode<false>, tmap, a);
+    e = cudaLaunchKernelEx(&lc, fsb_smem_encode, tmap, a);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "fsb_smem_encode launch");
     *launches = 1;
