@@ -140,6 +140,8 @@ struct SmemArgs {
   uint32_t slice0;             // first 64-B slice of the column range
   uint32_t sched_chunks, cont_base;
   uint32_t paired;             // 1: tiles come in adjacent-slice pairs, full 128-B line stores
+  uint32_t pair_tiles;         // paired: tiles per CTA run as pairs (even); the rest are tail singles
+  uint32_t tail_tiles;         // paired: single (unpaired) tiles after the pair rounds, over all CTAs
   uint32_t tmem_cols;          // TMEM columns allocated per CTA in paired mode (power of 2)
   uint32_t debug;              // FSB_DEBUG bits (profiling experiments only; 0 in production)
   uint32_t wait_ns;            // consumer sleep between probes of a tile's `ready` barrier
@@ -269,19 +271,31 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
   }
 }
 
-// Tile i of this CTA: (stripe, slice).  (Recomputed with two divisions per tile on purpose: an
-// incremental iterator kept ~8 more registers live across the consumers' item loop and made
-// config 4 6% slower, 0.597 -> 0.631 ms, profiles/r02/ab_r02o.txt.)  Unpaired: tile blockIdx.x + i*gridDim.x of S x nslices.
-// Paired: pair blockIdx.x + (i/2)*gridDim.x of S x nslices/2, slice 2*(pair % (nslices/2)) plus
-// (i&1), flipped on odd CTAs: half the SMs write their lines while the other half park, so the
-// HBM write stream stays even instead of pulsing with the tile pairs.
+// Tile i of this CTA: (stripe, slice).  Unpaired: tile blockIdx.x + i*gridDim.x of S x nslices.
+// Paired: tiles i < pair_tiles are pairs -- pair blockIdx.x + (i/2)*gridDim.x of S x nslices/2,
+// slice 2*(pair % (nslices/2)) plus (i&1), flipped on odd CTAs (half the SMs write their lines
+// while the other half park, so the HBM write stream stays even) -- and the pairs that do not
+// fill a last round of CTAs run as single unpaired tiles, one per CTA (tail_tiles of them), so no
+// CTA does a whole pair more than the mean (config 4 on 8 GPUs: 3.46 pairs per CTA on average
+// would otherwise take 4).  (Recomputed with two divisions per tile on purpose: an incremental
+// iterator kept ~8 more registers live across the consumers' item loop and made config 4 6%
+// slower, 0.597 -> 0.631 ms, profiles/r02/ab_r02o.txt.)
 __device__ __forceinline__ bool tile_of(const SmemArgs &a, uint32_t i, uint32_t &stripe, uint32_t &slice) {
   if (a.paired) {
-    const uint32_t pair = blockIdx.x + (i >> 1) * gridDim.x;
     const uint32_t nsp = a.nslices >> 1;
-    if (pair >= (a.ntiles >> 1)) return false;
+    uint32_t pair, odd;
+    if (i < a.pair_tiles) {
+      pair = blockIdx.x + (i >> 1) * gridDim.x;
+      if (pair >= (a.ntiles >> 1)) return false;
+      odd = (i ^ blockIdx.x) & 1;
+    } else {
+      const uint32_t q = blockIdx.x + (i - a.pair_tiles) * gridDim.x;  // single tile of the tail
+      if (q >= a.tail_tiles) return false;
+      pair = (a.pair_tiles >> 1) * gridDim.x + (q >> 1);
+      odd = q & 1;
+    }
     stripe = pair / nsp;
-    slice = a.slice0 + 2 * (pair % nsp) + ((i ^ blockIdx.x) & 1);
+    slice = a.slice0 + 2 * (pair % nsp) + odd;
     return true;
   }
   const uint32_t tile = blockIdx.x + i * gridDim.x;
@@ -465,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t stripe, slice;
   for (uint32_t i = 0; tile_of(a, i, stripe, slice); ++i) {
     const uint32_t b = i & 1, ph = (i >> 1) & 1;
-    const int mode = a.paired ? 1 + (i & 1) : 0;
+    const int mode = (a.paired && i < a.pair_tiles) ? 1 + (i & 1) : 0;
     const uint32_t first = (blockIdx.x & 1) ? kSliceBytes : 0;  // line offset of the pair's first tile
     // odd tiles of a pair read the partner half-group's schedule (its rows, their slice s+1)
     const uint32_t hsel = (mode == 2 ? half_id ^ 1 : half_id) * 16;
@@ -1123,6 +1137,22 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
       a.wait_ns = wns;
     }
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(a.paired ? tiles / 2 : tiles, g.sm_count));
+    a.pair_tiles = a.tail_tiles = 0;
+    if (a.paired) {
+      // pair rounds: every CTA gets npairs / grid pairs; a last partial round of R pairs runs as 2R
+      // single tiles when they fit one per CTA (2R <= grid), otherwise as pairs (ceil)
+      static const int tail_env = [] {
+        const char *e = std::getenv("FSB_TAIL_SINGLES");
+        return e ? std::atoi(e) : 1;
+      }();
+      const uint64_t npairs = tiles / 2, jfull = npairs / grid, rem = npairs % grid;
+      if (tail_env && rem && 2 * rem <= grid) {
+        a.pair_tiles = static_cast<uint32_t>(2 * jfull);
+        a.tail_tiles = static_cast<uint32_t>(2 * rem);
+      } else {
+        a.pair_tiles = static_cast<uint32_t>(2 * ((npairs + grid - 1) / grid));
+      }
+    }
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(grid);
     lc.blockDim = dim3(kThreads);

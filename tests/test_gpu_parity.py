@@ -4,6 +4,8 @@ Bar: bit-exact on every output byte (checks and coded symbols) -
 integer XOR.  Full-size configs are compared in full (the C oracle finishes them in
 seconds), in the launch configuration bench.py times.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -565,3 +567,33 @@ def test_many_wave_band_kernel_ragged(seed, t, S, dist):
     g.encode(d[1], chk[1], out, a, b)
     torch.cuda.synchronize()
     _assert_equal(out.cpu().numpy(), Y[1][a:b], "row range")
+
+
+@pytest.mark.parametrize("S", [5, 20, 77])
+def test_smem_pair_rounds_with_tail_singles(S):
+    """Paired SMEM tiles whose last partial round of pairs runs as single unpaired tiles (config 4
+    geometry, 32 pairs per stripe: S=5 -> 160 pairs = 1 round of 148 + 12 pairs as 24 singles;
+    S=20 -> 640 = 4 rounds + 48 pairs as 96 singles; S=77 -> 2464 = 16 rounds + 96 pairs, 2R > 148:
+    pairs) -- every stripe against the oracle."""
+    _need_gpu()
+    cfg = configs.get(4, stripes=S)
+    D, C, Y = _oracle_case(cfg)
+    _, c, y = _run(cfg, fsb.VARIANT_SMEM)
+    _assert_equal(c, C, "checks S=%d" % S)
+    _assert_equal(y, Y, "coded S=%d" % S)
+
+
+@pytest.mark.parametrize("band_cfg", ["0", "1", "2"])
+def test_band_kernel_instances_by_env(band_cfg):
+    """The other GLOBAL band-kernel instances FSB_BAND_CFG selects (read once per process, so each
+    runs in a fresh process): 0 = fsb_lt_band<4, 6, lazy> for every call, 1 = the round-1
+    fsb_lt_band<2, 8> for many-wave calls, 2 = <8, 4> -- config 5 in full against the oracle."""
+    _need_gpu()
+    import subprocess
+    import sys as _sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FSB_BAND_CFG=band_cfg)
+    r = subprocess.run([_sys.executable, os.path.join(root, "tools", "gpu", "check_cfg.py"), "5", "global"],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().endswith("ok"), r.stdout

@@ -16,12 +16,18 @@ from paper_1702_07409_b200 import configs, fsb, inputs  # noqa: E402
 cid = int(sys.argv[1])
 var = sys.argv[2] if len(sys.argv) > 2 else "auto"
 cfg = configs.get(cid)
-cache = "/tmp/oracle_c%d.npz" % cid
+go = oracle.generate_graph(cfg)
+# the oracle's output, cached under /tmp by a hash of the oracle's own graph and the config
+import hashlib  # noqa: E402
+h = hashlib.sha256()
+for arr in (go.pre_row_ptr, go.pre_col, go.lt_row_ptr, go.lt_col):
+    h.update(np.ascontiguousarray(arr, dtype="<i4").tobytes())
+h.update(repr(sorted((k, v) for k, v in cfg.items() if not isinstance(v, tuple))).encode())
+cache = "/tmp/oracle_c%d_%s.npz" % (cid, h.hexdigest()[:16])
 if os.path.exists(cache):
     z = np.load(cache)
     C, Y = z["C"], z["Y"]
 else:
-    go = oracle.generate_graph(cfg)
     C, Y = oracle.encode(go, inputs.stripe_data(cfg).numpy())
     np.savez(cache, C=C, Y=Y)
 g = fsb.Graph.create(cfg)
