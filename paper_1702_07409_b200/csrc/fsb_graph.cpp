@@ -610,4 +610,43 @@ void build_smem_schedule(Graph &g) {
   g.smem_eligible = true;
 }
 
+// Pack the LT rows into the fixed-size edge windows of fsb_lt_win (fsb_internal.h: LtWindows):
+// rows in order, a window closes when the next row would exceed 32 x regs edges (after padding
+// to a multiple of 4) or max_rows rows.  A row of more than 32 x regs - 3 edges fits no window:
+// then count = 0 and the band kernels take every call.
+void build_lt_windows(Graph &g, uint32_t max_rows, uint32_t regs) {
+  LtWindows &w = g.win;
+  w = LtWindows();
+  const uint32_t kWinEntries = 32 * regs;
+  w.entries = kWinEntries;
+  const uint32_t n = g.prm.n;
+  const std::vector<int32_t> &rp = g.lt_row_ptr;
+  if (max_rows == 0) return;
+  for (uint32_t j = 0; j < n; ++j)
+    if (static_cast<uint32_t>(rp[j + 1] - rp[j]) + 3 > kWinEntries) return;
+  uint32_t j = 0;
+  while (j < n) {
+    uint32_t j1 = j, cnt = 0;
+    while (j1 < n && j1 - j < max_rows) {
+      const uint32_t d = static_cast<uint32_t>(rp[j1 + 1] - rp[j1]);
+      if (((cnt + d + 3) & ~3u) > kWinEntries) break;
+      cnt += d;
+      ++j1;
+    }
+    const uint32_t padded = (cnt + 3) & ~3u, skip = padded - cnt;
+    const size_t base = w.ent.size();
+    w.ent.resize(base + kWinEntries, 0u);
+    for (uint32_t e = 0; e < skip; ++e) w.ent[base + e] = kWinSkip;
+    uint32_t e = skip;
+    for (uint32_t r = j; r < j1; ++r) {
+      for (int32_t x = rp[r]; x < rp[r + 1]; ++x) w.ent[base + e++] = static_cast<uint32_t>(g.lt_col[x]);
+      w.ent[base + e - 1] |= 0x80000000u;  // last edge of row r
+    }
+    w.hdr.push_back(j);
+    w.hdr.push_back(padded / 4);
+    j = j1;
+  }
+  w.count = static_cast<uint32_t>(w.hdr.size() / 2);
+}
+
 }  // namespace fsb

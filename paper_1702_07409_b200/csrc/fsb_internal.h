@@ -76,10 +76,26 @@ struct SmemSchedule {
   uint32_t pad_slots = 0;               // slots that read a zero row (parity / length padding)
 };
 
+// Fixed-size LT edge windows of the fsb_lt_win band kernel (built by build_lt_windows): window w
+// holds whole rows [hdr[w].x, next window's first row), at most `rows` of them, as marked edges
+// (bit 31 = last edge of a row) at ent[w * entries ...]; its edge count is padded to a multiple
+// of 4 with kWinSkip entries at the start; hdr[w].y = the window's batches of 4.  entries =
+// 32 x kWinRegs (one 32-bit register per lane per 32 edges).
+constexpr uint32_t kWinRegs = 3;
+constexpr uint32_t kWinRows = 12;
+constexpr uint32_t kWinSkip = 1u << 30;
+struct LtWindows {
+  std::vector<uint32_t> hdr;   // 2 words per window: first row, batches of 4
+  std::vector<uint32_t> ent;   // `entries` words per window
+  uint32_t entries = 0;        // edge slots per window (32 x registers per lane)
+  uint32_t count = 0;          // windows; 0 = some row does not fit a window (kernel not used)
+};
+
 struct DeviceBufs {
   int device = -1;
   int32_t *pre_row_ptr = nullptr, *pre_col = nullptr, *lt_row_ptr = nullptr, *lt_col = nullptr;
   uint32_t *lt_colf = nullptr;  // lt_col with bit 31 set on the last edge of each row
+  uint32_t *win_hdr = nullptr, *win_ent = nullptr;  // LtWindows on the device
   uint32_t *sched = nullptr;
   uint32_t *warp_info = nullptr;
   uint16_t *pre_slots = nullptr;
@@ -95,6 +111,7 @@ struct Graph {
   uint32_t max_degree = 0;
   bool smem_eligible = false;
   SmemSchedule sched;
+  LtWindows win;
   DeviceBufs dev;
   int32_t variant = FS_VARIANT_AUTO;
   int sm_count = 0;
@@ -109,6 +126,7 @@ fs_status generate_csr(Graph &g);
 fs_status validate_csr(const Graph &g);
 fs_status build_precode_levels(Graph &g);
 void build_smem_schedule(Graph &g);
+void build_lt_windows(Graph &g, uint32_t max_rows, uint32_t regs);
 
 // fsb_kernels.cu
 fs_status upload_graph(Graph &g);

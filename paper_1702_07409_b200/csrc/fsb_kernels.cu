@@ -757,6 +757,136 @@ __global__ void __launch_bounds__(kBT, kMinBlocks)
   }
 }
 
+// fsb_lt_win: the band kernel over fixed-size edge windows (round 2).  The host packs the LT rows
+// into windows of at most 32 x kWR marked edges and a few whole rows (fsb_internal.h: LtWindows);
+// a warp takes one (stripe, 512-B band, window), so the window's edges sit at
+// went[w * 32 * kWR] and its first row in whdr[w]: both loads depend only on the warp's unit
+// index and go out together, where fsb_lt_band4 first reads row_ptr and only then the edge
+// indices (two dependent L2 round trips before the first gather).  Each window's edge count is
+// padded to a multiple of 4 with skip entries at its start (bit 30), so every batch of 4 sits
+// aligned inside one 32-edge register and only the first batch is predicated.  A window may start
+// before row_begin or end after row_end (row-range calls, kRange): rows outside the range are
+// computed but not stored.
+template <int kB, bool kRange>
+__device__ __forceinline__ void win_batch(uint4 &acc, const uint32_t (&f)[kB], const uint4 (&v)[kB], uint8_t *&out,
+                                          uint32_t t, bool active, uint32_t lane, uint32_t &row, uint32_t rb,
+                                          uint32_t re) {
+  uint32_t sel = 0;
+#pragma unroll
+  for (int u = 0; u < kB; ++u) sel = lane == static_cast<uint32_t>(u) ? f[u] : sel;
+  const uint32_t ends = __ballot_sync(0xffffffffu, lane < static_cast<uint32_t>(kB) && static_cast<int32_t>(sel) < 0);
+  if (ends == 0u) {
+#pragma unroll
+    for (int u = 0; u + 1 < kB; u += 2) {
+      acc.x ^= v[u].x ^ v[u + 1].x;
+      acc.y ^= v[u].y ^ v[u + 1].y;
+      acc.z ^= v[u].z ^ v[u + 1].z;
+      acc.w ^= v[u].w ^ v[u + 1].w;
+    }
+    if (kB & 1) xor_into(acc, v[kB - 1]);
+  } else {
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      xor_into(acc, v[u]);
+      if (ends & (1u << u)) {
+        if (active && (!kRange || (row >= rb && row < re))) *reinterpret_cast<uint4 *>(out) = acc;
+        out += t;
+        if (kRange) ++row;
+        acc = make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+}
+
+template <int kWR, int kMinBlocks, int kBT, bool kRange, int kPrefetch>
+__global__ void __launch_bounds__(kBT, kMinBlocks)
+    fsb_lt_win(uint32_t S, uint32_t k, uint32_t t, uint32_t col0, uint32_t col1, uint32_t nbands, uint32_t w0,
+               uint32_t nwin, uint32_t row_begin, uint32_t row_end, const uint2 *__restrict__ whdr,
+               const uint32_t *__restrict__ went, const uint8_t *__restrict__ data, uint64_t data_stride,
+               const uint8_t *__restrict__ checks, uint64_t checks_stride, uint8_t *__restrict__ coded,
+               uint64_t coded_stride, uint32_t K) {
+  constexpr int kB = 4;  // gathers per batch; 8 batches per 32-edge register
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the precode launch (PDL)
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t unit = blockIdx.x * (kBT / 32) + (threadIdx.x >> 5);  // < 2^31 (host check)
+  const uint32_t w = w0 + unit % nwin;
+  const uint32_t rest = unit / nwin;
+  const uint32_t band = rest % nbands;
+  const uint32_t s = rest / nbands;
+  if (s >= S) return;
+  // the window: header and all its edge slots in one round trip
+  const uint32_t *we = went + static_cast<size_t>(w) * (32 * kWR);
+  const uint2 h = __ldg(&whdr[w]);
+  uint32_t cv[kWR];
+#pragma unroll
+  for (int r = 0; r < kWR; ++r) cv[r] = __ldg(&we[32 * r + lane]);
+  if (kPrefetch) {
+    // the next band's source block (the next stripe's first band after the last), 1/nwin of its
+    // K rows per window, so every 512-B row piece is requested into L2 once, spread over this
+    // band's sweep
+    uint32_t nband = band + 1, ns = s;
+    if (nband == nbands) { nband = 0; ++ns; }
+    const uint32_t wi = unit % nwin;
+    // kPrefetch 3: only the second half of the band's windows prefetch (2/nwin of the rows each)
+    if (ns < S && (kPrefetch != 3 || 2 * wi >= nwin)) {
+      const uint32_t part = kPrefetch == 3 ? 2 * wi - nwin : wi, parts = kPrefetch == 3 ? nwin - nwin / 2 : nwin;
+      const uint32_t m0 = static_cast<uint32_t>(static_cast<uint64_t>(part) * K / parts);
+      const uint32_t m1 = static_cast<uint32_t>(static_cast<uint64_t>(part + 1) * K / parts);
+      const uint32_t c = col0 + nband * kBandBytes;
+      const uint32_t bytes = min(kBandBytes, col1 - c) & ~15u;
+      if (kPrefetch == 2) {  // per 128-B line through the LSU: row (m0 + lane/4), line lane%4
+        for (uint32_t m = m0 + (lane >> 2); m < m1; m += 8) {
+          const uint32_t off = (lane & 3) * 128;
+          if (off < bytes) {
+            const uint8_t *p = (m < k ? data + ns * data_stride + static_cast<uint64_t>(m) * t
+                                      : checks + ns * checks_stride + static_cast<uint64_t>(m - k) * t) + c + off;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p) : "memory");
+          }
+        }
+      } else {
+        for (uint32_t m = m0 + lane; m < m1 && bytes; m += 32) {
+          const uint8_t *p = (m < k ? data + ns * data_stride + static_cast<uint64_t>(m) * t
+                                    : checks + ns * checks_stride + static_cast<uint64_t>(m - k) * t) + c;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+        }
+      }
+    }
+  }
+  const uint32_t byte_raw = col0 + band * kBandBytes + lane * 16;
+  const bool active = byte_raw < col1;
+  const uint32_t byte = active ? byte_raw : col0;
+  const uint8_t *dbase = data + s * data_stride + byte;
+  const uint8_t *cbase = checks + s * checks_stride + byte - static_cast<uint64_t>(k) * t;
+  uint32_t row = h.x;
+  const uint32_t nb = h.y;  // batches of 4 (>= 1)
+  uint8_t *out = coded + s * coded_stride + (static_cast<int64_t>(row) - static_cast<int64_t>(row_begin)) * t + byte_raw;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  {  // batch 0: its leading skip entries (bit 30) load nothing
+    uint32_t f[kB];
+    uint4 v[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      f[u] = __shfl_sync(0xffffffffu, cv[0], u);
+      v[u] = make_uint4(0, 0, 0, 0);
+      if (!(f[u] & kWinSkip)) v[u] = ldg16(src_addr(f[u], k, t, dbase, cbase));
+    }
+    win_batch<kB, kRange>(acc, f, v, out, t, active, lane, row, row_begin, row_end);
+  }
+#pragma unroll
+  for (int r = 0; r < kWR; ++r) {  // batches 8r .. 8r+7 live in register r
+    for (uint32_t b = (r == 0 ? 1 : 0); b < 8 && 8 * r + b < nb; ++b) {
+      uint32_t f[kB];
+      uint4 v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        f[u] = __shfl_sync(0xffffffffu, cv[r], b * kB + u);
+        v[u] = ldg16(src_addr(f[u], k, t, dbase, cbase));
+      }
+      win_batch<kB, kRange>(acc, f, v, out, t, active, lane, row, row_begin, row_end);
+    }
+  }
+}
+
 // ====================================================================== decoder (NEXT-1)
 // One DPG level (fsb_decode.cpp): row r recovers intermediate symbol target[r] of every stripe as
 // the XOR of its sources (intermediate rows recovered at earlier levels, or a received coded
@@ -958,6 +1088,8 @@ void free_device(Graph &g) {
   cudaFree(d.lt_row_ptr);
   cudaFree(d.lt_col);
   cudaFree(d.lt_colf);
+  cudaFree(d.win_hdr);
+  cudaFree(d.win_ent);
   cudaFree(d.sched);
   cudaFree(d.warp_info);
   cudaFree(d.pre_slots);
@@ -984,6 +1116,22 @@ fs_status upload_graph(Graph &g) {
     std::vector<uint32_t> colf(g.lt_col.begin(), g.lt_col.end());
     for (uint32_t j = 0; j < g.prm.n; ++j) colf[g.lt_row_ptr[j + 1] - 1] |= 0x80000000u;
     if ((st = upload(&g.dev.lt_colf, colf.data(), colf.size())) != FS_OK) return st;
+  }
+  {  // fixed-size edge windows for fsb_lt_win (FSB_WIN_ROWS: rows per window, 0 = none)
+    static const uint32_t win_rows = [] {
+      const char *e = std::getenv("FSB_WIN_ROWS");
+      return e ? static_cast<uint32_t>(std::atoi(e)) : kWinRows;
+    }();
+    static const uint32_t win_regs = [] {  // 32-edge registers per lane: 3, 4 or 5
+      const char *e = std::getenv("FSB_WIN_REGS");
+      const uint32_t r = e ? static_cast<uint32_t>(std::atoi(e)) : kWinRegs;
+      return r < 3 ? 3u : (r > 5 ? 5u : r);
+    }();
+    build_lt_windows(g, win_rows, win_regs);
+    if (g.win.count) {
+      if ((st = upload(&g.dev.win_hdr, g.win.hdr.data(), g.win.hdr.size())) != FS_OK) return st;
+      if ((st = upload(&g.dev.win_ent, g.win.ent.data(), g.win.ent.size())) != FS_OK) return st;
+    }
   }
   if (g.smem_eligible) {
     // two tile buffers + the schedule + the precode member rows + 6 mbarriers
@@ -1226,14 +1374,59 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
       blocks_launch = (units + kBand4Threads / 32 - 1) / (kBand4Threads / 32);
     }
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(static_cast<uint32_t>(blocks_launch));
-    lc.blockDim = dim3(block_threads);
-    lc.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = attr;
     lc.numAttrs = pdl_enabled() && prm.p ? 1 : 0;  // overlaps the precode launch
+    lc.stream = stream;
+    if (((band_cfg == 5 && !few_waves) || band_cfg == 6) && g.win.count) {
+      // fixed-size edge windows: the windows holding rows [row_begin, row_end)
+      const uint32_t *hw = g.win.hdr.data();
+      uint32_t lo = 0, hi = g.win.count;  // last window whose first row <= row_begin
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (hw[2 * mid] <= row_begin) lo = mid; else hi = mid;
+      }
+      const uint32_t w0 = lo;
+      lo = w0; hi = g.win.count;           // last window whose first row < row_end
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (hw[2 * mid] < row_end) lo = mid; else hi = mid;
+      }
+      const uint32_t nwin = lo + 1 - w0;
+      const uint64_t wunits = static_cast<uint64_t>(S) * nbands * nwin;
+      const uint64_t wblocks = (wunits + kBand4Threads / 32 - 1) / (kBand4Threads / 32);
+      if (wblocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
+      lc.gridDim = dim3(static_cast<uint32_t>(wblocks));
+      lc.blockDim = dim3(kBand4Threads);
+      // full-row calls store every row (no range predicate: one register less, no spill)
+      const bool full = row_begin == 0 && row_end == prm.n;
+      static const int win_pf = [] {  // FSB_WIN_PF=1: prefetch the next band's source into L2
+        const char *e = std::getenv("FSB_WIN_PF");
+        return e ? std::atoi(e) : 0;
+      }();
+      auto wk = full ? fsb_lt_win<3, 24, kBand4Threads, false, 0> : fsb_lt_win<3, 24, kBand4Threads, true, 0>;
+      if (win_pf == 1) wk = full ? fsb_lt_win<3, 24, kBand4Threads, false, 1> : fsb_lt_win<3, 24, kBand4Threads, true, 1>;
+      if (win_pf == 2) wk = full ? fsb_lt_win<3, 24, kBand4Threads, false, 2> : fsb_lt_win<3, 24, kBand4Threads, true, 2>;
+      if (win_pf == 3) wk = full ? fsb_lt_win<3, 24, kBand4Threads, false, 3> : fsb_lt_win<3, 24, kBand4Threads, true, 3>;
+      if (g.win.entries == 128)
+        wk = full ? fsb_lt_win<4, 20, kBand4Threads, false, 0> : fsb_lt_win<4, 20, kBand4Threads, true, 0>;
+      if (g.win.entries == 160)
+        wk = full ? fsb_lt_win<5, 20, kBand4Threads, false, 0> : fsb_lt_win<5, 20, kBand4Threads, true, 0>;
+      e = cudaLaunchKernelEx(&lc, wk, S, prm.k, static_cast<uint32_t>(prm.t),
+                             static_cast<uint32_t>(col_begin), static_cast<uint32_t>(col_end), nbands, w0, nwin,
+                             row_begin, row_end, reinterpret_cast<const uint2 *>(g.dev.win_hdr),
+                             static_cast<const uint32_t *>(g.dev.win_ent), data, data_stride,
+                             static_cast<const uint8_t *>(checks), checks_stride, coded, coded_stride,
+                             prm.k + prm.p);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(e, "fsb_lt_win launch");
+      ++*launches;
+      return FS_OK;
+    }
+    lc.gridDim = dim3(static_cast<uint32_t>(blocks_launch));
+    lc.blockDim = dim3(block_threads);
     e = cudaLaunchKernelEx(&lc, kern, S, prm.k, static_cast<uint32_t>(prm.t), static_cast<uint32_t>(col_begin),
                            static_cast<uint32_t>(col_end), nbands, row_begin, nrows, band_rows,
                            static_cast<const int32_t *>(g.dev.lt_row_ptr), static_cast<const uint32_t *>(g.dev.lt_colf),

@@ -583,17 +583,35 @@ def test_smem_pair_rounds_with_tail_singles(S):
     _assert_equal(y, Y, "coded S=%d" % S)
 
 
-@pytest.mark.parametrize("band_cfg", ["0", "1", "2"])
+@pytest.mark.parametrize("band_cfg", ["0", "1", "2", "4"])
 def test_band_kernel_instances_by_env(band_cfg):
     """The other GLOBAL band-kernel instances FSB_BAND_CFG selects (read once per process, so each
     runs in a fresh process): 0 = fsb_lt_band<4, 6, lazy> for every call, 1 = the round-1
-    fsb_lt_band<2, 8> for many-wave calls, 2 = <8, 4> -- config 5 in full against the oracle."""
+    fsb_lt_band<2, 8> for many-wave calls, 2 = <8, 4>, 4 = fsb_lt_band4 (round 2 before the edge
+    windows) -- config 5 in full against the oracle."""
     _need_gpu()
     import subprocess
     import sys as _sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, FSB_BAND_CFG=band_cfg)
     r = subprocess.run([_sys.executable, os.path.join(root, "tools", "gpu", "check_cfg.py"), "5", "global"],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().endswith("ok"), r.stdout
+
+
+@pytest.mark.parametrize("regs,rows", [("3", "8"), ("3", "16"), ("4", "16"), ("5", "20"), ("5", "32")])
+def test_window_kernel_shapes(regs, rows):
+    """fsb_lt_win (fixed-size edge windows, FSB_BAND_CFG=5) with 96 / 128 / 160-edge windows and
+    8-32 rows per window (FSB_WIN_REGS / FSB_WIN_ROWS, read once per process): config 5's full-row
+    encode and its row ranges -- rank partitions G = 2, 3 and ranges that start and end inside a
+    window (rows computed but not stored) -- bit-exact against the oracle (tools/gpu/check_win.py)."""
+    _need_gpu()
+    import subprocess
+    import sys as _sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FSB_BAND_CFG="5", FSB_WIN_REGS=regs, FSB_WIN_ROWS=rows)
+    r = subprocess.run([_sys.executable, os.path.join(root, "tools", "gpu", "check_win.py"), "5"],
                        capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip().endswith("ok"), r.stdout
