@@ -439,7 +439,9 @@ def main():
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
             "algorithmic_bytes_per_launch": b_hbm, "peak_source": peak_src,
-            "kernel": "fsb_smem_encode" if smem_kernel else "fsb_precode_global+fsb_lt_band",
+            "kernel": "fsb_smem_encode" if smem_kernel else (
+                "fsb_precode_global+fsb_lt_win" if inf.get("lt_windows") and os.environ.get("FSB_BAND_CFG", "5") == "5"
+                else "fsb_precode_global+fsb_lt_band"),
             "timing": "CUDA events on the launching stream, mean per step (%d launch%s per step)"
                       % (launches_per_step, "" if smem_kernel else "es"),
             "gather": {"bytes_per_launch": b_gather,

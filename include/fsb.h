@@ -148,6 +148,8 @@ typedef struct {
   uint32_t sched_steps_max;  /* SMEM schedule: gather slots of the most loaded warp per tile  */
   uint32_t sched_steps_avg;  /* SMEM schedule: mean gather slots per warp per tile (rounded)  */
   int32_t device;            /* CUDA device of the device copy, -1 for host-only graphs       */
+  uint32_t lt_windows;       /* fixed-size LT edge windows of the GLOBAL window kernel (0: none,
+                                e.g. a row of more than 93 edges, or a host-only graph)          */
 } fs_graph_info;
 
 FSB_API fs_status fs_graph_get_info(const fs_graph *g, fs_graph_info *info);

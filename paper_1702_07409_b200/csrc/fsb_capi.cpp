@@ -150,6 +150,7 @@ fs_status fs_graph_get_info(const fs_graph *h, fs_graph_info *info) {
   info->sched_steps_max = g.sched.steps_max;
   info->sched_steps_avg = (g.sched.steps_total + fsb::kConsumerWarps / 2) / fsb::kConsumerWarps;
   info->device = g.dev.device;
+  info->lt_windows = g.win.count;
   return FS_OK;
 }
 

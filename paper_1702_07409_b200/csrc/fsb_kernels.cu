@@ -798,13 +798,13 @@ __device__ __forceinline__ void win_batch(uint4 &acc, const uint32_t (&f)[kB], c
   }
 }
 
-template <int kWR, int kMinBlocks, int kBT, bool kRange, int kPrefetch>
+template <int kWR, int kMinBlocks, int kBT, bool kRange>
 __global__ void __launch_bounds__(kBT, kMinBlocks)
     fsb_lt_win(uint32_t S, uint32_t k, uint32_t t, uint32_t col0, uint32_t col1, uint32_t nbands, uint32_t w0,
                uint32_t nwin, uint32_t row_begin, uint32_t row_end, const uint2 *__restrict__ whdr,
                const uint32_t *__restrict__ went, const uint8_t *__restrict__ data, uint64_t data_stride,
                const uint8_t *__restrict__ checks, uint64_t checks_stride, uint8_t *__restrict__ coded,
-               uint64_t coded_stride, uint32_t K) {
+               uint64_t coded_stride) {
   constexpr int kB = 4;  // gathers per batch; 8 batches per 32-edge register
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the precode launch (PDL)
   const uint32_t lane = threadIdx.x & 31;
@@ -820,38 +820,6 @@ __global__ void __launch_bounds__(kBT, kMinBlocks)
   uint32_t cv[kWR];
 #pragma unroll
   for (int r = 0; r < kWR; ++r) cv[r] = __ldg(&we[32 * r + lane]);
-  if (kPrefetch) {
-    // the next band's source block (the next stripe's first band after the last), 1/nwin of its
-    // K rows per window, so every 512-B row piece is requested into L2 once, spread over this
-    // band's sweep
-    uint32_t nband = band + 1, ns = s;
-    if (nband == nbands) { nband = 0; ++ns; }
-    const uint32_t wi = unit % nwin;
-    // kPrefetch 3: only the second half of the band's windows prefetch (2/nwin of the rows each)
-    if (ns < S && (kPrefetch != 3 || 2 * wi >= nwin)) {
-      const uint32_t part = kPrefetch == 3 ? 2 * wi - nwin : wi, parts = kPrefetch == 3 ? nwin - nwin / 2 : nwin;
-      const uint32_t m0 = static_cast<uint32_t>(static_cast<uint64_t>(part) * K / parts);
-      const uint32_t m1 = static_cast<uint32_t>(static_cast<uint64_t>(part + 1) * K / parts);
-      const uint32_t c = col0 + nband * kBandBytes;
-      const uint32_t bytes = min(kBandBytes, col1 - c) & ~15u;
-      if (kPrefetch == 2) {  // per 128-B line through the LSU: row (m0 + lane/4), line lane%4
-        for (uint32_t m = m0 + (lane >> 2); m < m1; m += 8) {
-          const uint32_t off = (lane & 3) * 128;
-          if (off < bytes) {
-            const uint8_t *p = (m < k ? data + ns * data_stride + static_cast<uint64_t>(m) * t
-                                      : checks + ns * checks_stride + static_cast<uint64_t>(m - k) * t) + c + off;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(p) : "memory");
-          }
-        }
-      } else {
-        for (uint32_t m = m0 + lane; m < m1 && bytes; m += 32) {
-          const uint8_t *p = (m < k ? data + ns * data_stride + static_cast<uint64_t>(m) * t
-                                    : checks + ns * checks_stride + static_cast<uint64_t>(m - k) * t) + c;
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-        }
-      }
-    }
-  }
   const uint32_t byte_raw = col0 + band * kBandBytes + lane * 16;
   const bool active = byte_raw < col1;
   const uint32_t byte = active ? byte_raw : col0;
@@ -1352,23 +1320,26 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     const uint64_t units = static_cast<uint64_t>(S) * nbands * ((nrows + band_rows - 1) / band_rows);
     const uint64_t blocks = (units + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
     if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
-    // Many-wave calls (config 5: 13 waves) take fsb_lt_band4: 4 gathers per batch, 2-warp blocks,
-    // 48 warps per SM (same-box A/B, tools/gpu/ab/run_multi.sh, profiles/r02: 0.252 ms vs 0.278
-    // for fsb_lt_band<2, 8> with 8-warp blocks; 2-warp blocks alone 0.263 -> 0.252).  Calls of
-    // only a few waves end on their heaviest rows' serial gather chains and keep the lazily
-    // waiting fsb_lt_band<4, 6> (config 3: 35.2 -> 30.1 us vs 2 in flight).  FSB_BAND_CFG: 4 =
-    // this rule (default), 1 = fsb_lt_band<2, 8> for many-wave calls (round-1 kernel), 0 = always
-    // <4, 6>, 2 = <8, 4>.
+    // Every call whose rows fit the edge windows takes fsb_lt_win: the edges packed into fixed-size
+    // windows, 4 gathers per batch, 2-warp blocks, 48 warps per SM (same-box A/B, profiles/r02:
+    // config 5 0.221 ms vs 0.251 for fsb_lt_band4 and 0.278 for the round-1 fsb_lt_band<2, 8>;
+    // config 3, a few-wave call that ends on its heaviest rows' serial gather chains, 21.6 vs
+    // 30.0 us for fsb_lt_band<4, 6, lazy>).  Without windows (a row of more than 93 edges):
+    // fsb_lt_band4 for many-wave calls, fsb_lt_band<4, 6, lazy> for few-wave ones.  FSB_BAND_CFG:
+    // 5 = this rule (default), 4 = never windows, 1 = fsb_lt_band<2, 8> for every call (the
+    // round-1 many-wave kernel), 0 = always <4, 6>, 2 = always <8, 4>.
     static const int band_cfg = [] {
       const char *e = std::getenv("FSB_BAND_CFG");
-      return e ? std::atoi(e) : 4;
+      return e ? std::atoi(e) : 5;
     }();
     const bool few_waves = units < 4ull * g.sm_count * 64;
-    auto kern = (band_cfg == 0 || (band_cfg == 4 && few_waves)) ? fsb_lt_band<4, 6, true> : fsb_lt_band<2, 8, false>;
+    const bool use_win = g.win.count && band_cfg == 5;
+    auto kern = fsb_lt_band<4, 6, true>;
+    if (band_cfg == 1) kern = fsb_lt_band<2, 8, false>;
     if (band_cfg == 2) kern = fsb_lt_band<8, 4, false>;
     uint64_t blocks_launch = blocks;
     uint32_t block_threads = kGlobalThreads;
-    if (band_cfg == 4 && !few_waves) {
+    if ((band_cfg == 4 || band_cfg == 5) && !few_waves && !use_win) {
       kern = fsb_lt_band4<4, 24, kBand4Threads>;
       block_threads = kBand4Threads;
       blocks_launch = (units + kBand4Threads / 32 - 1) / (kBand4Threads / 32);
@@ -1380,7 +1351,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     lc.attrs = attr;
     lc.numAttrs = pdl_enabled() && prm.p ? 1 : 0;  // overlaps the precode launch
     lc.stream = stream;
-    if (((band_cfg == 5 && !few_waves) || band_cfg == 6) && g.win.count) {
+    if (use_win) {
       // fixed-size edge windows: the windows holding rows [row_begin, row_end)
       const uint32_t *hw = g.win.hdr.data();
       uint32_t lo = 0, hi = g.win.count;  // last window whose first row <= row_begin
@@ -1402,24 +1373,16 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
       lc.blockDim = dim3(kBand4Threads);
       // full-row calls store every row (no range predicate: one register less, no spill)
       const bool full = row_begin == 0 && row_end == prm.n;
-      static const int win_pf = [] {  // FSB_WIN_PF=1: prefetch the next band's source into L2
-        const char *e = std::getenv("FSB_WIN_PF");
-        return e ? std::atoi(e) : 0;
-      }();
-      auto wk = full ? fsb_lt_win<3, 24, kBand4Threads, false, 0> : fsb_lt_win<3, 24, kBand4Threads, true, 0>;
-      if (win_pf == 1) wk = full ? fsb_lt_win<3, 24, kBand4Threads, false, 1> : fsb_lt_win<3, 24, kBand4Threads, true, 1>;
-      if (win_pf == 2) wk = full ? fsb_lt_win<3, 24, kBand4Threads, false, 2> : fsb_lt_win<3, 24, kBand4Threads, true, 2>;
-      if (win_pf == 3) wk = full ? fsb_lt_win<3, 24, kBand4Threads, false, 3> : fsb_lt_win<3, 24, kBand4Threads, true, 3>;
+      auto wk = full ? fsb_lt_win<3, 24, kBand4Threads, false> : fsb_lt_win<3, 24, kBand4Threads, true>;
       if (g.win.entries == 128)
-        wk = full ? fsb_lt_win<4, 20, kBand4Threads, false, 0> : fsb_lt_win<4, 20, kBand4Threads, true, 0>;
+        wk = full ? fsb_lt_win<4, 20, kBand4Threads, false> : fsb_lt_win<4, 20, kBand4Threads, true>;
       if (g.win.entries == 160)
-        wk = full ? fsb_lt_win<5, 20, kBand4Threads, false, 0> : fsb_lt_win<5, 20, kBand4Threads, true, 0>;
+        wk = full ? fsb_lt_win<5, 20, kBand4Threads, false> : fsb_lt_win<5, 20, kBand4Threads, true>;
       e = cudaLaunchKernelEx(&lc, wk, S, prm.k, static_cast<uint32_t>(prm.t),
                              static_cast<uint32_t>(col_begin), static_cast<uint32_t>(col_end), nbands, w0, nwin,
                              row_begin, row_end, reinterpret_cast<const uint2 *>(g.dev.win_hdr),
                              static_cast<const uint32_t *>(g.dev.win_ent), data, data_stride,
-                             static_cast<const uint8_t *>(checks), checks_stride, coded, coded_stride,
-                             prm.k + prm.p);
+                             static_cast<const uint8_t *>(checks), checks_stride, coded, coded_stride);
       if (e == cudaSuccess) e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(e, "fsb_lt_win launch");
       ++*launches;

@@ -54,7 +54,7 @@ class fs_graph_info(ctypes.Structure):
                 ("variant", ctypes.c_int32), ("smem_eligible", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_uint32), ("sched_bytes", ctypes.c_uint32),
                 ("sched_steps_max", ctypes.c_uint32), ("sched_steps_avg", ctypes.c_uint32),
-                ("device", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("lt_windows", ctypes.c_uint32)]
 
 
 class fs_checks_info(ctypes.Structure):
