@@ -767,6 +767,32 @@ __global__ void __launch_bounds__(kBT, kMinBlocks)
 // aligned inside one 32-edge register and only the first batch is predicated.  A window may start
 // before row_begin or end after row_end (row-range calls, kRange): rows outside the range are
 // computed but not stored.
+#ifndef FSB_WIN_POLICY
+#define FSB_WIN_POLICY 1  // 1 = source loads with an L2 evict_last policy (default; A/B: config 3 21.6 -> 19.5 us, config 5 unchanged); 2 = row stores evict_first (experiments)
+#endif
+__device__ __forceinline__ uint4 ldg16_pol(const uint8_t *p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg16_pol(uint8_t *p, const uint4 &v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 template <int kB, bool kRange>
 __device__ __forceinline__ void win_batch(uint4 &acc, const uint32_t (&f)[kB], const uint4 (&v)[kB], uint8_t *&out,
                                           uint32_t t, bool active, uint32_t lane, uint32_t &row, uint32_t rb,
@@ -789,7 +815,13 @@ __device__ __forceinline__ void win_batch(uint4 &acc, const uint32_t (&f)[kB], c
     for (int u = 0; u < kB; ++u) {
       xor_into(acc, v[u]);
       if (ends & (1u << u)) {
-        if (active && (!kRange || (row >= rb && row < re))) *reinterpret_cast<uint4 *>(out) = acc;
+        if (active && (!kRange || (row >= rb && row < re))) {
+#if FSB_WIN_POLICY & 2
+          stg16_pol(out, acc, policy_evict_first());
+#else
+          *reinterpret_cast<uint4 *>(out) = acc;
+#endif
+        }
         out += t;
         if (kRange) ++row;
         acc = make_uint4(0, 0, 0, 0);
@@ -806,6 +838,12 @@ __global__ void __launch_bounds__(kBT, kMinBlocks)
                const uint8_t *__restrict__ checks, uint64_t checks_stride, uint8_t *__restrict__ coded,
                uint64_t coded_stride) {
   constexpr int kB = 4;  // gathers per batch; 8 batches per 32-edge register
+#if FSB_WIN_POLICY & 1
+  const uint64_t lpol = policy_evict_last();
+#define WIN_LDG(p) ldg16_pol((p), lpol)
+#else
+#define WIN_LDG(p) ldg16(p)
+#endif
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the precode launch (PDL)
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t unit = blockIdx.x * (kBT / 32) + (threadIdx.x >> 5);  // < 2^31 (host check)
@@ -836,7 +874,7 @@ __global__ void __launch_bounds__(kBT, kMinBlocks)
     for (int u = 0; u < kB; ++u) {
       f[u] = __shfl_sync(0xffffffffu, cv[0], u);
       v[u] = make_uint4(0, 0, 0, 0);
-      if (!(f[u] & kWinSkip)) v[u] = ldg16(src_addr(f[u], k, t, dbase, cbase));
+      if (!(f[u] & kWinSkip)) v[u] = WIN_LDG(src_addr(f[u], k, t, dbase, cbase));
     }
     win_batch<kB, kRange>(acc, f, v, out, t, active, lane, row, row_begin, row_end);
   }
@@ -848,7 +886,7 @@ __global__ void __launch_bounds__(kBT, kMinBlocks)
 #pragma unroll
       for (int u = 0; u < kB; ++u) {
         f[u] = __shfl_sync(0xffffffffu, cv[r], b * kB + u);
-        v[u] = ldg16(src_addr(f[u], k, t, dbase, cbase));
+        v[u] = WIN_LDG(src_addr(f[u], k, t, dbase, cbase));
       }
       win_batch<kB, kRange>(acc, f, v, out, t, active, lane, row, row_begin, row_end);
     }
