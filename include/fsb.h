@@ -149,7 +149,7 @@ typedef struct {
   uint32_t sched_steps_avg;  /* SMEM schedule: mean gather slots per warp per tile (rounded)  */
   int32_t device;            /* CUDA device of the device copy, -1 for host-only graphs       */
   uint32_t lt_windows;       /* fixed-size LT edge windows of the GLOBAL window kernel (0: none,
-                                e.g. a row of more than 93 edges, or a host-only graph)          */
+                                i.e. a row of more than 93 edges; fs_graph_windows)              */
 } fs_graph_info;
 
 FSB_API fs_status fs_graph_get_info(const fs_graph *g, fs_graph_info *info);
@@ -213,6 +213,16 @@ FSB_API fs_status fs_encode_host(const fs_graph *g, uint32_t num_stripes,
  * row 0xFFFF = no output) and slots 0..5 in words 1..3; slots 6..L-1 follow in the conts stream,
  * 8 per chunk.  In every step, half 0 of a group reads an even row iff half 1 reads an odd one
  * (shared-memory bank rule).  FS_EUNSUPPORTED when the graph is not SMEM-eligible.          */
+/* The fixed-size LT edge windows of the GLOBAL window kernel (host views, owned by g): window w
+ * (w < *count) covers the LT rows [hdr[2w], hdr[2w+2]) (the last window ends at n); hdr[2w+1] =
+ * its batches of 4 edges; its *entries edge slots ent[w * *entries ...] hold the rows' column
+ * indices in row order, bit 31 set on each row's last edge, preceded by (4 - edges % 4) % 4
+ * padding slots with bit 30 set (kernel skips them); the rest of the slots are 0.  Windows hold
+ * at most 12 rows (FSB_WIN_ROWS) and 96 edge slots.  FS_EUNSUPPORTED when the graph has no
+ * windows (a row of more than 93 edges).                                                    */
+FSB_API fs_status fs_graph_windows(const fs_graph *g, const uint32_t **hdr, const uint32_t **ent,
+                                   uint32_t *count, uint32_t *entries);
+
 FSB_API fs_status fs_graph_schedule(const fs_graph *g, const uint32_t **words, uint64_t *nwords,
                                     uint32_t *cont_base, const uint32_t **warp_info, uint32_t *nwarps,
                                     uint32_t *kpad, uint32_t *zero_even);

@@ -1,4 +1,5 @@
 // C ABI of libfsb200.so (include/fsb.h): argument validation, ownership, error reporting.
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <new>
@@ -26,6 +27,19 @@ fs_status finish_create(fs_graph *h, uint32_t flags, fs_graph **out) {
     return lv;
   }
   fsb::build_smem_schedule(g);
+  {  // fixed-size edge windows of the GLOBAL LT kernel (FSB_WIN_ROWS: rows per window, 0 = none;
+     // FSB_WIN_REGS: 32-edge registers per lane, 3..5)
+    static const uint32_t win_rows = [] {
+      const char *e = std::getenv("FSB_WIN_ROWS");
+      return e ? static_cast<uint32_t>(std::atoi(e)) : fsb::kWinRows;
+    }();
+    static const uint32_t win_regs = [] {
+      const char *e = std::getenv("FSB_WIN_REGS");
+      const uint32_t r = e ? static_cast<uint32_t>(std::atoi(e)) : fsb::kWinRegs;
+      return r < 3 ? 3u : (r > 5 ? 5u : r);
+    }();
+    fsb::build_lt_windows(g, win_rows, win_regs);
+  }
   if (!(flags & FS_GRAPH_HOST_ONLY)) {
     fs_status st = fsb::upload_graph(g);
     if (st != FS_OK) {
@@ -290,6 +304,18 @@ fs_status fs_graph_schedule(const fs_graph *h, const uint32_t **words, uint64_t 
   if (nwarps) *nwarps = fsb::kConsumerWarps;
   if (kpad) *kpad = g.sched.kpad;
   if (zero_even) *zero_even = g.sched.zero_even;
+  return FS_OK;
+}
+
+fs_status fs_graph_windows(const fs_graph *h, const uint32_t **hdr, const uint32_t **ent, uint32_t *count,
+                           uint32_t *entries) {
+  if (!h) { set_error("null graph"); return FS_EINVAL; }
+  const fsb::Graph &g = h->g;
+  if (!g.win.count) { set_error("graph has no LT edge windows"); return FS_EUNSUPPORTED; }
+  if (hdr) *hdr = g.win.hdr.data();
+  if (ent) *ent = g.win.ent.data();
+  if (count) *count = g.win.count;
+  if (entries) *entries = g.win.entries;
   return FS_OK;
 }
 

@@ -24,7 +24,7 @@ VARIANT_AUTO, VARIANT_SMEM, VARIANT_GLOBAL = 0, 1, 2
 # Every symbol include/fsb.h declares (checked by tests/test_capi.py).
 EXPORTS = ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get_info",
            "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_last_launch_count",
-           "fs_free", "fs_last_error", "fs_version", "fs_graph_schedule", "fs_debug_counters",
+           "fs_free", "fs_last_error", "fs_version", "fs_graph_schedule", "fs_graph_windows", "fs_debug_counters",
            "fs_decode_plan_create", "fs_decode_plan_info", "fs_decode_plan_state", "fs_decode",
            "fs_decode_plan_free", "fs_encode_range", "fs_checks_create", "fs_checks_from_data",
            "fs_checks_data", "fs_checks_info_get", "fs_checks_free", "fs_repair_plan_create",
@@ -103,8 +103,10 @@ def lib():
         L.fs_encode_host.restype = ctypes.c_int
         L.fs_graph_schedule.argtypes = [P, PP, ctypes.POINTER(u64), ctypes.POINTER(u32), PP,
                                         ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u32)]
+        L.fs_graph_windows.argtypes = [P, PP, PP, ctypes.POINTER(u32), ctypes.POINTER(u32)]
         for f in ("fs_graph_create", "fs_graph_from_csr", "fs_graph_csr", "fs_graph_get_info",
-                  "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_graph_schedule"):
+                  "fs_graph_set_variant", "fs_encode", "fs_encode_stripes", "fs_graph_schedule",
+                  "fs_graph_windows"):
             getattr(L, f).restype = ctypes.c_int
         L.fs_decode_plan_create.argtypes = [P, P, u32, PP]
         L.fs_decode_plan_info.argtypes = [P, ctypes.POINTER(fs_decode_info)]
@@ -281,6 +283,18 @@ class Graph:
         info = np.ctypeslib.as_array(ctypes.cast(wi, ctypes.POINTER(ctypes.c_uint32)),
                                      (3 * nwarps.value,)).copy()
         return words, cb.value, info.reshape(-1, 3), kpad.value, z0.value
+
+    def windows(self):
+        """(hdr uint32[count, 2], ent uint32[count, entries]) of the GLOBAL kernel's LT edge
+        windows (copies; format in include/fsb.h)."""
+        hp, ep = ctypes.c_void_p(), ctypes.c_void_p()
+        cnt, ne = ctypes.c_uint32(), ctypes.c_uint32()
+        _check(lib().fs_graph_windows(self._h, ctypes.byref(hp), ctypes.byref(ep), ctypes.byref(cnt),
+                                      ctypes.byref(ne)))
+        hdr = np.ctypeslib.as_array(ctypes.cast(hp, ctypes.POINTER(ctypes.c_uint32)), (2 * cnt.value,)).copy()
+        ent = np.ctypeslib.as_array(ctypes.cast(ep, ctypes.POINTER(ctypes.c_uint32)),
+                                    (cnt.value * ne.value,)).copy()
+        return hdr.reshape(-1, 2), ent.reshape(cnt.value, ne.value)
 
     def extend(self, extra_files, host_only=False):
         """fs_graph_extend (update): the graph with extra_files more output files."""

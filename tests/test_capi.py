@@ -240,6 +240,56 @@ def test_smem_schedule_covers_every_edge(cid):
         assert rows[j] == want
 
 
+def _replay_windows(hdr, ent, n):
+    """Host replay of the GLOBAL window kernel (fsb_lt_win) over fs_graph_windows: the rows each
+    window produces, in order, each as its list of source indices."""
+    rows = []
+    for w in range(hdr.shape[0]):
+        r0, nb = int(hdr[w, 0]), int(hdr[w, 1])
+        r1 = int(hdr[w + 1, 0]) if w + 1 < hdr.shape[0] else n
+        assert 1 <= nb and 4 * nb <= ent.shape[1]
+        assert 1 <= r1 - r0 <= 12
+        assert r0 == (len(rows))                   # windows tile the rows in order
+        cur = []
+        for e in range(4 * nb):
+            f = int(ent[w, e])
+            if f & (1 << 30):                      # skip slot: only before the first edge
+                assert e < 4 and not cur and not (f & (1 << 31))
+                continue
+            cur.append(f & 0x7FFFFFFF)
+            if f & (1 << 31):
+                rows.append(cur)
+                cur = []
+        assert not cur                             # the window ends on a row end
+        assert np.all(ent[w, 4 * nb:] == 0)
+        assert len(rows) == r1
+    return rows
+
+
+@pytest.mark.parametrize("cid", [3, 5])
+def test_lt_windows_cover_every_edge(cid):
+    """fs_graph_windows: replaying the window kernel's walk yields every LT row exactly once, in
+    order, with exactly its CSR neighbours (bit-exact encode needs nothing more)."""
+    c = configs.get(cid)
+    g = fsb.Graph.create(c, host_only=True)
+    assert g.info()["lt_windows"] > 0
+    hdr, ent = g.windows()
+    _, _, lt_rp, lt_c = g.csr()
+    rows = _replay_windows(hdr, ent, c["n"])
+    assert len(rows) == c["n"]
+    for j in range(c["n"]):
+        assert rows[j] == list(lt_c[lt_rp[j]:lt_rp[j + 1]])
+
+
+def test_lt_windows_absent_for_heavy_rows():
+    """A graph with a row of more than 93 edges has no windows (the band kernels run it)."""
+    c = configs.get(4)                             # RSD, max degree 251
+    g = fsb.Graph.create(c, host_only=True)
+    assert g.info()["max_degree"] > 93 and g.info()["lt_windows"] == 0
+    with pytest.raises(fsb.FsError):
+        g.windows()
+
+
 ARRAY_CFGS = [
     dict(k=962, p=74, d_p=0, n=1280, t=4096, dist=configs.RSD, rsd_c=0.1, rsd_delta=0.05, seed=6),
     dict(k=837, p=93, d_p=0, n=1100, t=128, dist=configs.FINITE, seed=7,
