@@ -174,8 +174,6 @@ constexpr uint32_t kSrcCoded = 1u << 30;
 constexpr uint32_t kSrcWork = 1u << 29;   // a workspace row (inactivation decoding, Z rows)
 constexpr uint32_t kSrcIndex = kSrcWork - 1;
 constexpr uint32_t kSrcLast = 1u << 31;
-constexpr uint32_t kSrcSkip = kSrcCoded | kSrcWork;  // window padding entry (fsb_dpg_win): no source
-constexpr uint32_t kDpgWinTargets = 16;             // target slots per level window (rows <= this)
 struct DecodePlan {
   uint32_t k = 0, p = 0, n = 0, K = 0;
   uint64_t t = 0;
@@ -194,15 +192,6 @@ struct DecodePlan {
   int32_t *d_target = nullptr, *d_src_ptr = nullptr;
   uint32_t *d_src = nullptr;
   int sm_count = 0;
-  // fixed-size source windows of the level kernel fsb_dpg_win (built by upload_decode_plan): per
-  // level L, windows [win_level[L], win_level[L+1]) hold its rows in order, each window <= 96
-  // flagged sources (padded to a multiple of 4 with kSrcSkip entries at the start) and <=
-  // kDpgWinTargets rows; win_nb[w] = batches of 4, win_tgt[w * kDpgWinTargets + i] = target of
-  // its row i.  win_level empty: no windows (a row of more than 93 sources).
-  std::vector<uint32_t> win_level, win_nb, win_ent;
-  std::vector<int32_t> win_tgt;
-  uint32_t *d_win_nb = nullptr, *d_win_ent = nullptr;
-  int32_t *d_win_tgt = nullptr;
   // the level launches captured once as a CUDA graph per (S, buffers, strides) and replayed
   // (fsb_kernels.cu; created by upload_decode_plan, guarded by its own mutex)
   std::shared_ptr<struct PlanGraphCache> gcache;

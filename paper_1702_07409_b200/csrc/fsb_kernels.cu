@@ -972,71 +972,6 @@ __global__ void __launch_bounds__(kGlobalThreads, kMinBlocks)
   }
 }
 
-// fsb_dpg_win: one DPG level over fixed-size source windows (the plan's rows of the level packed
-// by upload_decode_plan, like fsb_lt_win's edge windows): a warp takes one (stripe, 512-B band,
-// window); the window's batch count, its 96 flagged sources and its rows' targets are addressed
-// by the unit index alone, so they arrive in one round of independent loads (fsb_dpg_level reads
-// target / src_ptr and only then the sources).  Sources and targets as in fsb_dpg_level.
-template <int kMinBlocks>
-__global__ void __launch_bounds__(kBand4Threads, kMinBlocks)
-    fsb_dpg_win(uint32_t S, uint32_t t, uint32_t nbands, uint32_t w0, uint32_t nwin, const uint32_t *__restrict__ wnb,
-                const uint32_t *__restrict__ went, const int32_t *__restrict__ wtgt, uint8_t *coded,
-                uint64_t coded_stride, uint8_t *inter, uint64_t inter_stride, uint8_t *work, uint64_t work_stride,
-                uint32_t rev) {
-  constexpr int kB = 4;
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t total = static_cast<uint64_t>(S) * nbands * nwin;
-  uint64_t unit = static_cast<uint64_t>(blockIdx.x) * (kBand4Threads / 32) + (threadIdx.x >> 5);
-  if (unit >= total) return;
-  if (rev) unit = total - 1 - unit;  // serpentine (as fsb_dpg_level)
-  const uint32_t w = w0 + static_cast<uint32_t>(unit % nwin);
-  unit /= nwin;
-  const uint32_t band = static_cast<uint32_t>(unit % nbands);
-  const uint64_t s = unit / nbands;
-  const uint32_t *we = went + static_cast<size_t>(w) * 96;
-  const uint32_t nb = __ldg(&wnb[w]);
-  const uint32_t cv0 = __ldg(&we[lane]), cv1 = __ldg(&we[32 + lane]), cv2 = __ldg(&we[64 + lane]);
-  const int32_t tg = __ldg(&wtgt[static_cast<size_t>(w) * kDpgWinTargets + (lane & (kDpgWinTargets - 1))]);
-  const uint32_t byte_raw = band * kBandBytes + lane * 16;
-  const bool active = byte_raw < t;
-  const uint32_t byte = active ? byte_raw : 0;
-  const uint8_t *ibase = inter + s * inter_stride + byte;
-  const uint8_t *cbase = coded + s * coded_stride + byte;
-  const uint8_t *wbase = work + s * work_stride + byte;
-  uint32_t cur = 0;
-  uint4 acc = make_uint4(0, 0, 0, 0);
-  for (uint32_t b = 0; b < nb; ++b) {
-    const uint32_t cv = b < 8 ? cv0 : (b < 16 ? cv1 : cv2);  // warp-uniform
-    uint32_t fl[kB];
-    uint4 v[kB];
-#pragma unroll
-    for (int u = 0; u < kB; ++u) {
-      fl[u] = __shfl_sync(0xffffffffu, cv, ((b * kB) & 31) + u);
-      const uint32_t m = fl[u] & kSrcIndex;
-      const uint8_t *b0 = (fl[u] & kSrcCoded) ? cbase : (fl[u] & kSrcWork) ? wbase : ibase;
-      v[u] = make_uint4(0, 0, 0, 0);
-      if ((fl[u] & kSrcSkip) != kSrcSkip)  // (only batch 0 has skip entries)
-        asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
-                     : "l"(b0 + static_cast<uint64_t>(m) * t));
-    }
-#pragma unroll
-    for (int u = 0; u < kB; ++u) {
-      xor_into(acc, v[u]);
-      if ((fl[u] & kSrcLast) && (fl[u] & kSrcSkip) != kSrcSkip) {  // warp-uniform: row complete
-        const uint32_t f = static_cast<uint32_t>(__shfl_sync(0xffffffffu, tg, cur));
-        // (an active lane's load base is its store base: byte == byte_raw)
-        const uint8_t *ob = (f & kSrcCoded) ? cbase : (f & kSrcWork) ? wbase : ibase;
-        if (active) *reinterpret_cast<uint4 *>(const_cast<uint8_t *>(ob) + static_cast<uint64_t>(f & kSrcIndex) * t) = acc;
-        acc = make_uint4(0, 0, 0, 0);
-        ++cur;
-      }
-    }
-  }
-}
-
 // Levels of long rows (late decode levels, repair / update rows: tens to hundreds of sources):
 // in fsb_dpg_level a warp walks a row's sources one 512-B gather after another, a serial chain
 // of L2 / HBM round trips.  Here a warp covers a 128-B band of its rows as four 8-lane groups:
@@ -1520,49 +1455,6 @@ fs_status upload_decode_plan(DecodePlan &pl) {
   if ((st = upload(&pl.d_target, pl.target.data(), pl.target.size())) != FS_OK) return st;
   if ((st = upload(&pl.d_src_ptr, pl.src_ptr.data(), pl.src_ptr.size())) != FS_OK) return st;
   if ((st = upload(&pl.d_src, pl.src.data(), pl.src.size())) != FS_OK) return st;
-  {  // source windows per level for fsb_dpg_win (a level with a row of > 93 sources: none)
-    const uint32_t nbands = static_cast<uint32_t>((pl.t + kBandBytes - 1) / kBandBytes);
-    pl.win_level.assign(1, 0);
-    pl.win_nb.clear();
-    pl.win_ent.clear();
-    pl.win_tgt.clear();
-    for (size_t L = 0; L + 1 < pl.level_ptr.size(); ++L) {
-      const uint32_t r0 = pl.level_ptr[L], r1 = pl.level_ptr[L + 1];
-      bool fits = true;
-      for (uint32_t r = r0; r < r1 && fits; ++r) fits = pl.src_ptr[r + 1] - pl.src_ptr[r] + 3 <= 96;
-      if (fits) {
-        // rows per window: up to 8, fewer when the level (one stripe) gives < 64 warps per SM
-        const uint32_t rpw = static_cast<uint32_t>(std::max<uint64_t>(
-            1, std::min<uint64_t>(8, static_cast<uint64_t>(r1 - r0) * nbands / (64ull * pl.sm_count))));
-        for (uint32_t r = r0; r < r1;) {
-          uint32_t r2 = r, cnt = 0;
-          while (r2 < r1 && r2 - r < rpw) {
-            const uint32_t d = static_cast<uint32_t>(pl.src_ptr[r2 + 1] - pl.src_ptr[r2]);
-            if (((cnt + d + 3) & ~3u) > 96) break;
-            cnt += d;
-            ++r2;
-          }
-          const uint32_t padded = (cnt + 3) & ~3u;
-          const size_t base = pl.win_ent.size();
-          pl.win_ent.resize(base + 96, kSrcSkip);
-          uint32_t e = padded - cnt;  // skip entries first
-          for (uint32_t q = r; q < r2; ++q)
-            for (int32_t x = pl.src_ptr[q]; x < pl.src_ptr[q + 1]; ++x) pl.win_ent[base + e++] = pl.src[x];
-          pl.win_nb.push_back(padded / 4);
-          const size_t tb = pl.win_tgt.size();
-          pl.win_tgt.resize(tb + kDpgWinTargets, 0);
-          for (uint32_t q = r; q < r2; ++q) pl.win_tgt[tb + (q - r)] = pl.target[q];
-          r = r2;
-        }
-      }
-      pl.win_level.push_back(static_cast<uint32_t>(pl.win_nb.size()));
-    }
-    if (!pl.win_nb.empty()) {
-      if ((st = upload(&pl.d_win_nb, pl.win_nb.data(), pl.win_nb.size())) != FS_OK) return st;
-      if ((st = upload(&pl.d_win_ent, pl.win_ent.data(), pl.win_ent.size())) != FS_OK) return st;
-      if ((st = upload(&pl.d_win_tgt, pl.win_tgt.data(), pl.win_tgt.size())) != FS_OK) return st;
-    }
-  }
   pl.gcache = std::make_shared<PlanGraphCache>();
   return FS_OK;
 }
@@ -1575,11 +1467,6 @@ void free_decode_plan(DecodePlan &pl) {
   cudaFree(pl.d_target);
   cudaFree(pl.d_src_ptr);
   cudaFree(pl.d_src);
-  cudaFree(pl.d_win_nb);
-  cudaFree(pl.d_win_ent);
-  cudaFree(pl.d_win_tgt);
-  pl.d_win_nb = pl.d_win_ent = nullptr;
-  pl.d_win_tgt = nullptr;
   pl.gcache.reset();  // graph exec and capture stream of this device
   if (prev >= 0) cudaSetDevice(prev);
   pl.d_target = pl.d_src_ptr = nullptr;
@@ -1718,7 +1605,6 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
     }();
     uint32_t nb = nbands, br = band_rows;
     uint64_t nunits = units;
-    bool qkern = false;
     if (q_min && nsrc >= static_cast<uint64_t>(q_min) * nrows) {
       const uint32_t qnb = static_cast<uint32_t>((pl.t + kQBandBytes - 1) / kQBandBytes);
       const uint32_t qbr = q_rows > 0 ? std::min<uint32_t>(kBandRowsMax, static_cast<uint32_t>(q_rows))
@@ -1727,41 +1613,7 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
       if (q_min == 1 || qunits >= 4ull * pl.sm_count * 48) {  // FSB_DPG_Q=1: every level (tests)
         kern = q_cfg == 0 ? fsb_dpg_level_q<8, 4> : q_cfg == 2 ? fsb_dpg_level_q<2, 8> : fsb_dpg_level_q<4, 6>;
         nb = qnb, br = qbr, nunits = qunits;
-        qkern = true;
       }
-    }
-    // Levels whose rows fit the plan's source windows (all but the long-row levels above) take
-    // fsb_dpg_win (FSB_DPG_WIN=0: never)
-    static const int dpg_win = [] {
-      const char *e = std::getenv("FSB_DPG_WIN");
-      return e ? std::atoi(e) : 1;
-    }();
-    const uint32_t wl0 = pl.win_level.empty() ? 0 : pl.win_level[L];
-    const uint32_t wl1 = pl.win_level.empty() ? 0 : pl.win_level[L + 1];
-    if (dpg_win && !qkern && wl1 > wl0) {
-      const uint64_t wunits = static_cast<uint64_t>(S) * nbands * (wl1 - wl0);
-      const uint64_t wblocks = (wunits + kBand4Threads / 32 - 1) / (kBand4Threads / 32);
-      if (wblocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }
-      cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3(static_cast<uint32_t>(wblocks));
-      lc.blockDim = dim3(kBand4Threads);
-      lc.stream = stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = 1;
-      lc.attrs = attr;
-      lc.numAttrs = pdl_enabled() && L > 0 ? 1 : 0;
-      // FSB_DPG_WIN=2: 40 warps per SM (48 registers, no spill) instead of 48 (40 registers)
-      cudaError_t e = cudaLaunchKernelEx(&lc, dpg_win == 2 ? fsb_dpg_win<20> : fsb_dpg_win<24>, S, static_cast<uint32_t>(pl.t), nbands, wl0, wl1 - wl0,
-                                         static_cast<const uint32_t *>(pl.d_win_nb),
-                                         static_cast<const uint32_t *>(pl.d_win_ent),
-                                         static_cast<const int32_t *>(pl.d_win_tgt), coded, coded_stride, inter,
-                                         inter_stride, work, work_stride,
-                                         serpentine() ? static_cast<uint32_t>(L & 1) : 0u);
-      if (e == cudaSuccess) e = cudaGetLastError();
-      if (e != cudaSuccess) return cuda_fail(e, "fsb_dpg_win launch");
-      ++*launches;
-      continue;
     }
     const uint64_t blocks = (nunits + kGlobalThreads / 32 - 1) / (kGlobalThreads / 32);
     if (blocks >= (1ull << 31)) { set_error("launch too large"); return FS_EINVAL; }

@@ -247,22 +247,3 @@ def test_gpu_decode_eliminate_random_graphs(seed):
         rec = ostate != 0
         assert np.array_equal(I[s][rec], oI[rec])
 
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("win", ["0", "2"])
-def test_level_kernel_instances_by_env(win):
-    """The level kernels FSB_DPG_WIN selects (read once per process, so each runs in a fresh
-    pytest process): 0 = fsb_dpg_level for every level (no source windows), 2 = fsb_dpg_win at 40
-    warps per SM -- the GPU decode and repair parity tests against the oracle."""
-    import os
-    import subprocess
-    import sys as _sys
-    if not torch.cuda.is_available():
-        pytest.skip("needs a GPU")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, FSB_DPG_WIN=win)
-    r = subprocess.run([_sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x",
-                        os.path.join(root, "tests", "test_decode.py") + "::test_gpu_decode_matches_oracle",
-                        os.path.join(root, "tests", "test_repair.py") + "::test_gpu_repair_parity"],
-                       capture_output=True, text=True, env=env, timeout=1200, cwd=root)
-    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
