@@ -227,7 +227,7 @@ def _simulate_schedule(g, c):
     return rows, kpad
 
 
-@pytest.mark.parametrize("cid", [1, 2, 4])
+@pytest.mark.parametrize("cid", [1, 2, 4, 6, 7])
 def test_smem_schedule_covers_every_edge(cid):
     c = configs.get(cid)
     g = fsb.Graph.create(c, host_only=True)
