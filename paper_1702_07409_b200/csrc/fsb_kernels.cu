@@ -893,112 +893,6 @@ __global__ void __launch_bounds__(kBT, kMinBlocks)
   }
 }
 
-// fsb_lt_win32: fsb_lt_win over 1-KB bands, 32 B per lane: each source gather is one 256-bit
-// load per lane (LDG.256, a warp load = 8 full lines) and each row leaves as one 256-bit store, so
-// a warp issues half the load, shuffle and address instructions per byte of fsb_lt_win.  kB
-// gathers per batch (2: the same bytes in flight per warp as fsb_lt_win's 4 x 16 B).  Requires
-// 32-B aligned columns and strides.
-struct U8x32 {
-  uint4 lo, hi;
-};
-__device__ __forceinline__ U8x32 ldg32_pol(const uint8_t *p, uint64_t pol) {
-  U8x32 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
-               : "=r"(v.lo.x), "=r"(v.lo.y), "=r"(v.lo.z), "=r"(v.lo.w), "=r"(v.hi.x), "=r"(v.hi.y), "=r"(v.hi.z),
-                 "=r"(v.hi.w)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void stg32(uint8_t *p, const U8x32 &v) {
-  asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v.lo.x), "r"(v.lo.y),
-               "r"(v.lo.z), "r"(v.lo.w), "r"(v.hi.x), "r"(v.hi.y), "r"(v.hi.z), "r"(v.hi.w)
-               : "memory");
-}
-constexpr uint32_t kBand32Bytes = 1024;
-
-template <int kB, bool kRange>
-__device__ __forceinline__ void win32_batch(U8x32 &acc, const uint32_t (&f)[kB], const U8x32 (&v)[kB], uint8_t *&out,
-                                            uint32_t t, bool active, uint32_t lane, uint32_t &row, uint32_t rb,
-                                            uint32_t re) {
-  uint32_t sel = 0;
-#pragma unroll
-  for (int u = 0; u < kB; ++u) sel = lane == static_cast<uint32_t>(u) ? f[u] : sel;
-  const uint32_t ends = __ballot_sync(0xffffffffu, lane < static_cast<uint32_t>(kB) && static_cast<int32_t>(sel) < 0);
-#pragma unroll
-  for (int u = 0; u < kB; ++u) {
-    xor_into(acc.lo, v[u].lo);
-    xor_into(acc.hi, v[u].hi);
-    if (ends & (1u << u)) {
-      if (active && (!kRange || (row >= rb && row < re))) stg32(out, acc);
-      out += t;
-      if (kRange) ++row;
-      acc.lo = make_uint4(0, 0, 0, 0);
-      acc.hi = make_uint4(0, 0, 0, 0);
-    }
-  }
-}
-
-template <int kB, int kMinBlocks, bool kRange>
-__global__ void __launch_bounds__(kBand4Threads, kMinBlocks)
-    fsb_lt_win32(uint32_t S, uint32_t k, uint32_t t, uint32_t col0, uint32_t col1, uint32_t nbands, uint32_t w0,
-                 uint32_t nwin, uint32_t row_begin, uint32_t row_end, const uint2 *__restrict__ whdr,
-                 const uint32_t *__restrict__ went, const uint8_t *__restrict__ data, uint64_t data_stride,
-                 const uint8_t *__restrict__ checks, uint64_t checks_stride, uint8_t *__restrict__ coded,
-                 uint64_t coded_stride) {
-  static_assert(kB == 2 || kB == 4, "batches must tile the 4-aligned windows");
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the precode launch (PDL)
-  const uint64_t lpol = policy_evict_last();
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t unit = blockIdx.x * (kBand4Threads / 32) + (threadIdx.x >> 5);
-  const uint32_t w = w0 + unit % nwin;
-  const uint32_t rest = unit / nwin;
-  const uint32_t band = rest % nbands;
-  const uint32_t s = rest / nbands;
-  if (s >= S) return;
-  const uint32_t *we = went + static_cast<size_t>(w) * 96;
-  const uint2 h = __ldg(&whdr[w]);
-  uint32_t cv[3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r) cv[r] = __ldg(&we[32 * r + lane]);
-  const uint32_t byte_raw = col0 + band * kBand32Bytes + lane * 32;
-  const bool active = byte_raw < col1;
-  const uint32_t byte = active ? byte_raw : col0;
-  const uint8_t *dbase = data + s * data_stride + byte;
-  const uint8_t *cbase = checks + s * checks_stride + byte - static_cast<uint64_t>(k) * t;
-  uint32_t row = h.x;
-  const uint32_t ne = 4 * h.y;  // edge slots (multiple of 4), skip slots first
-  uint8_t *out = coded + s * coded_stride + (static_cast<int64_t>(row) - static_cast<int64_t>(row_begin)) * t + byte_raw;
-  U8x32 acc;
-  acc.lo = acc.hi = make_uint4(0, 0, 0, 0);
-  {  // the first 4 slots: skip entries (bit 30) load nothing
-#pragma unroll
-    for (int b0 = 0; b0 < 4; b0 += kB) {
-      uint32_t f[kB];
-      U8x32 v[kB];
-#pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        f[u] = __shfl_sync(0xffffffffu, cv[0], b0 + u);
-        v[u].lo = v[u].hi = make_uint4(0, 0, 0, 0);
-        if (!(f[u] & kWinSkip)) v[u] = ldg32_pol(src_addr(f[u], k, t, dbase, cbase), lpol);
-      }
-      win32_batch<kB, kRange>(acc, f, v, out, t, active, lane, row, row_begin, row_end);
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    for (uint32_t e = (r == 0 ? 4 : 0); e < 32 && 32 * r + e < ne; e += kB) {
-      uint32_t f[kB];
-      U8x32 v[kB];
-#pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        f[u] = __shfl_sync(0xffffffffu, cv[r], e + u);
-        v[u] = ldg32_pol(src_addr(f[u], k, t, dbase, cbase), lpol);
-      }
-      win32_batch<kB, kRange>(acc, f, v, out, t, active, lane, row, row_begin, row_end);
-    }
-  }
-}
-
 // ====================================================================== decoder (NEXT-1)
 // One DPG level (fsb_decode.cpp): row r recovers intermediate symbol target[r] of every stripe as
 // the XOR of its sources (intermediate rows recovered at earlier levels, or a received coded
@@ -1510,25 +1404,8 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
         wk = full ? fsb_lt_win<4, 20, kBand4Threads, false> : fsb_lt_win<4, 20, kBand4Threads, true>;
       if (g.win.entries == 160)
         wk = full ? fsb_lt_win<5, 20, kBand4Threads, false> : fsb_lt_win<5, 20, kBand4Threads, true>;
-      // FSB_WIN_V8 (experiments): 1-KB bands, 256-bit gathers (1: 2 per batch, 2: 4 per batch)
-      static const int win_v8 = [] {
-        const char *e = std::getenv("FSB_WIN_V8");
-        return e ? std::atoi(e) : 0;
-      }();
-      uint32_t wbands = nbands;
-      const bool v8ok = win_v8 && g.win.entries == 96 && col_begin % 32 == 0 && prm.t % 32 == 0 &&
-                        data_stride % 32 == 0 && checks_stride % 32 == 0 && coded_stride % 32 == 0 &&
-                        reinterpret_cast<uintptr_t>(data) % 32 == 0 && reinterpret_cast<uintptr_t>(coded) % 32 == 0 &&
-                        (prm.p == 0 || reinterpret_cast<uintptr_t>(checks) % 32 == 0);
-      if (v8ok) {
-        wbands = static_cast<uint32_t>((col_end - col_begin + kBand32Bytes - 1) / kBand32Bytes);
-        if (win_v8 == 1) wk = full ? fsb_lt_win32<2, 20, false> : fsb_lt_win32<2, 20, true>;
-        else wk = full ? fsb_lt_win32<4, 16, false> : fsb_lt_win32<4, 16, true>;
-        const uint64_t wu = static_cast<uint64_t>(S) * wbands * nwin;
-        lc.gridDim = dim3(static_cast<uint32_t>((wu + kBand4Threads / 32 - 1) / (kBand4Threads / 32)));
-      }
       e = cudaLaunchKernelEx(&lc, wk, S, prm.k, static_cast<uint32_t>(prm.t),
-                             static_cast<uint32_t>(col_begin), static_cast<uint32_t>(col_end), wbands, w0, nwin,
+                             static_cast<uint32_t>(col_begin), static_cast<uint32_t>(col_end), nbands, w0, nwin,
                              row_begin, row_end, reinterpret_cast<const uint2 *>(g.dev.win_hdr),
                              static_cast<const uint32_t *>(g.dev.win_ent), data, data_stride,
                              static_cast<const uint8_t *>(checks), checks_stride, coded, coded_stride);
