@@ -162,7 +162,7 @@ fs_status fs_graph_get_info(const fs_graph *h, fs_graph_info *info) {
   info->smem_bytes = g.smem_bytes;
   info->sched_bytes = static_cast<uint32_t>(g.sched.words.size() * 4);
   info->sched_steps_max = g.sched.steps_max;
-  info->sched_steps_avg = (g.sched.steps_total + fsb::kConsumerWarps / 2) / fsb::kConsumerWarps;
+  info->sched_steps_avg = (g.sched.steps_total + g.sched.nconsumer / 2) / std::max<uint32_t>(g.sched.nconsumer, 1);
   info->device = g.dev.device;
   info->lt_windows = g.win.count;
   return FS_OK;
@@ -301,7 +301,7 @@ fs_status fs_graph_schedule(const fs_graph *h, const uint32_t **words, uint64_t 
   if (nwords) *nwords = g.sched.words.size();
   if (cont_base) *cont_base = g.sched.cont_base;
   if (warp_info) *warp_info = g.sched.warp_info.data();
-  if (nwarps) *nwarps = fsb::kConsumerWarps;
+  if (nwarps) *nwarps = g.sched.nconsumer;
   if (kpad) *kpad = g.sched.kpad;
   if (zero_even) *zero_even = g.sched.zero_even;
   return FS_OK;

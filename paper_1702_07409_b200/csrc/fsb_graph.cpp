@@ -344,6 +344,18 @@ void build_smem_schedule(Graph &g) {
   SmemSchedule &s = g.sched;
   s = SmemSchedule();
   g.smem_eligible = false;
+  // warps for the precode (FSB_PRECODE_WARPS = 3..7 overrides): 3, or 5 when the precode is >= 5%
+  // of the tile's gathers (array precode).  Same-box A/B (profiles/r02/ab_r02aj_precode_warps.txt):
+  // config 6 (13.5%) 0.758 -> 0.717 ms with 5; configs 4 and 7 (0.4%) fastest with 3.
+  {
+    static const int pw_env = [] {
+      const char *e = std::getenv("FSB_PRECODE_WARPS");
+      return e ? std::atoi(e) : 0;
+    }();
+    int pw = g.pre_col.size() * 20 >= g.lt_col.size() ? 5 : kPrecodeWarps;
+    if (pw_env >= 3 && pw_env <= 7) pw = pw_env;
+    s.nconsumer = static_cast<uint32_t>(kConsumerWarps + kPrecodeWarps - pw);
+  }
   const uint32_t k = g.prm.k, p = g.prm.p, n = g.prm.n;
   s.kpad = (k + kUnitRows - 1) / kUnitRows * kUnitRows;
   s.zero_even = (s.kpad + p + 1) & ~1u;
@@ -528,8 +540,9 @@ void build_smem_schedule(Graph &g) {
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost(items[a]) > cost(items[b]); });
   using Load = std::pair<uint64_t, int>;
   std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-  for (int w = 0; w < kConsumerWarps; ++w) heap.push({0, w});
-  std::vector<std::vector<uint32_t>> per_warp(kConsumerWarps);
+  const int ncw = static_cast<int>(s.nconsumer);
+  for (int w = 0; w < ncw; ++w) heap.push({0, w});
+  std::vector<std::vector<uint32_t>> per_warp(ncw);
   for (uint32_t idx : order) {
     Load l = heap.top();
     heap.pop();
@@ -548,7 +561,7 @@ void build_smem_schedule(Graph &g) {
   }
 #endif
   // emit the two chunk streams, warp after warp (32 words per chunk; half-group h: words 4h..4h+3)
-  s.warp_info.assign(kConsumerWarps * 3, 0);
+  s.warp_info.assign(ncw * 3, 0);
   std::vector<uint32_t> heads, conts;
   auto put = [](uint32_t &word, uint32_t i, uint16_t v) {  // slot i of a word pair position
     const uint32_t sh = (i & 1) ? kSlotHiShift : 0;
@@ -556,7 +569,7 @@ void build_smem_schedule(Graph &g) {
   };
   const uint32_t wpc = kChunkBytes / 4;  // words per chunk
   s.steps_max = s.steps_total = s.pad_slots = 0;
-  for (int w = 0; w < kConsumerWarps; ++w) {
+  for (int w = 0; w < ncw; ++w) {
     s.warp_info[w * 3 + 0] = static_cast<uint32_t>(per_warp[w].size());
     s.warp_info[w * 3 + 1] = static_cast<uint32_t>(heads.size() / wpc);
     s.warp_info[w * 3 + 2] = static_cast<uint32_t>(conts.size() / wpc);

@@ -66,7 +66,9 @@ constexpr uint32_t kMaxSmemSlots = (1u << kSlotBits) - 1;  // tile rows (data + 
 struct SmemSchedule {
   std::vector<uint32_t> words;          // heads stream (+pad) then conts stream (+pad), uint32 words
   uint32_t cont_base = 0;               // first chunk of the conts stream in `words`
-  std::vector<uint32_t> warp_info;      // kConsumerWarps x {items, head_off, cont_off} (chunks)
+  std::vector<uint32_t> warp_info;      // nconsumer x {items, head_off, cont_off} (chunks)
+  uint32_t nconsumer = kConsumerWarps;  // consumer warps; the other kConsumerWarps + kPrecodeWarps
+                                        // - nconsumer warps (besides the TMA warp) run the precode
   std::vector<uint16_t> pre_slots;      // p * d_p data rows
   uint32_t kpad = 0;                    // data rows rounded up to kUnitRows
   uint32_t zero_even = 0;               // tile rows of the two all-zero padding rows

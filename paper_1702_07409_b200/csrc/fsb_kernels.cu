@@ -91,8 +91,8 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void consumer_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+__device__ __forceinline__ void consumer_bar(uint32_t nconsumer) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nconsumer * 32) : "memory");
 }
 __device__ __forceinline__ void xor_into(uint4 &a, const uint4 &b) {
   a.x ^= b.x;
@@ -127,7 +127,7 @@ __device__ __forceinline__ uint4 tmem_ld16(uint32_t taddr) {
 __device__ unsigned long long g_debug_counters[2 * 32];
 struct SmemArgs {
   const uint4 *sched;          // heads ++ conts chunk streams (fsb_internal.h: SmemSchedule)
-  const uint32_t *warp_info;   // kConsumerWarps x {items, head_off, cont_off}
+  const uint32_t *warp_info;   // nc x {items, head_off, cont_off}
   const uint16_t *pre_slots;   // p * d_p tile rows (data, or an earlier check)
   const uint32_t *pre_level_ptr;  // precode levels (nlevels+1 row offsets)
   uint32_t pre_levels;
@@ -145,6 +145,7 @@ struct SmemArgs {
   uint32_t tmem_cols;          // TMEM columns allocated per CTA in paired mode (power of 2)
   uint32_t debug;              // FSB_DEBUG bits (profiling experiments only; 0 in production)
   uint32_t wait_ns;            // consumer sleep between probes of a tile's `ready` barrier
+  uint32_t nc;                 // consumer warps (0..nc-1); warp nc = TMA; warps nc+1.. = precode
 };
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -308,10 +309,12 @@ __device__ __forceinline__ bool tile_of(const SmemArgs &a, uint32_t i, uint32_t 
 // Persistent encode kernel, one CTA per SM.  Shared memory: two tile buffers (tile_units x 4 KiB
 // each), the LT schedule, the precode member rows, then the mbarriers and the TMEM address.
 // Warp roles:
-//   TMA warp (kConsumerWarps): lane 0 streams each tile's data rows in by TMA (box kUnitRows x 64 B);
-//   precode warps (the last kPrecodeWarps): the tile's p checks (PAPER.md:91 step (1)) from shared
+//   TMA warp (warp nc; nc = 24 consumer warps unless the graph's precode asks for more precode
+//     warps, SmemSchedule::nconsumer): lane 0 streams each tile's data rows in by TMA (box
+//     kUnitRows x 64 B);
+//   precode warps (the last 28 - 1 - nc): the tile's p checks (PAPER.md:91 step (1)) from shared
 //     memory into the buffer's check rows and to HBM, level by level, then `ready`;
-//   consumer warps (0..kConsumerWarps-1): every LT row (PAPER.md:91 step (2)) of the tile as a
+//   consumer warps (0..nc-1): every LT row (PAPER.md:91 step (2)) of the tile as a
 //     register XOR of 64-B rows gathered from shared memory (lt_item: 64-B stores unpaired,
 //     TMEM-parked halves and full 128-B lines paired).
 // Buffers alternate (tile i uses buffer i&1), so tile i+1 streams in while tile i computes, and a
@@ -336,14 +339,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
 
-  if (warp == kConsumerWarps && lane == 0) {
+  const int nc = static_cast<int>(a.nc);
+  const uint32_t npw = kConsumerWarps + kPrecodeWarps - a.nc;  // precode warps
+  if (warp == nc && lane == 0) {
     // the TMA thread: barriers, then -- once the previous grid in the stream has completed (this
     // prologue may overlap its tail: programmatic dependent launch) -- tile 0's loads, issued
     // while the other threads stage the schedule
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&full[b]), 1);
       mbar_init(smem_u32(&ready[b]), 1);
-      mbar_init(smem_u32(&empty[b]), kConsumerWarps);
+      mbar_init(smem_u32(&empty[b]), a.nc);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  if (warp == kConsumerWarps) {
+  if (warp == nc) {
     // ---------------------------------------------------------------- TMA warp (one lane)
     if (lane == 0) {
       uint32_t stripe, slice;
@@ -412,12 +417,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     return;
   }
-  if (warp > kConsumerWarps) {
+  if (warp > nc) {
     // ----------------------------------------------------------- precode warps (a3, Check #1)
     // After a tile's rows land: its p checks (PAPER.md:91 step (1)) from shared memory into the
     // buffer's check rows and to HBM, level by level (Alg 2 checks read earlier checks), then
     // `ready`.  Separate from the TMA warp so the next tile's loads never wait for this work.
-    const uint32_t pw = warp - kConsumerWarps - 1;                  // precode warp 0..kPrecodeWarps-1
+    const uint32_t pw = warp - nc - 1;                              // precode warp 0..npw-1
     const uint32_t half_id = pw * kHalvesPerWarp + (lane >> 2), lane4 = lane & 3;
     uint32_t stripe, slice;
     const long long pt0 = (a.debug & 2) ? clock64() : 0;
@@ -434,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t col_off = static_cast<uint64_t>(slice) * kSliceBytes + lane4 * 16;
       for (uint32_t L = 0; L < a.pre_levels; ++L) {
         const uint32_t c0 = __ldg(&a.pre_level_ptr[L]), c1 = __ldg(&a.pre_level_ptr[L + 1]);
-        for (uint32_t c = c0 + half_id; c < c1; c += kHalvesPerWarp * kPrecodeWarps) {
+        for (uint32_t c = c0 + half_id; c < c1; c += kHalvesPerWarp * npw) {
           uint4 acc = make_uint4(0, 0, 0, 0);
           const uint16_t *ps = pre_s + c * a.d_p;  // member rows, staged in shared memory
           uint32_t e = 0;
@@ -453,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           st_stream(a.checks + stripe * a.checks_stride + c * a.t + col_off, acc);
         }
         // this level's check rows before the next level reads them (all precode warps)
-        asm volatile("bar.sync 2, %0;" ::"n"(kPrecodeWarps * 32) : "memory");
+        asm volatile("bar.sync 2, %0;" ::"r"(npw * 32) : "memory");
       }
       if (pw == 0 && lane == 0) mbar_arrive(smem_u32(&ready[b]));  // release: data + checks visible
     }
@@ -511,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2 + 1], static_cast<unsigned long long>(clock64() - t_start));
   if (a.paired) {  // all consumer warps are done with TMEM; warp 0 frees it
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    consumer_bar();
+    consumer_bar(a.nc);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 0)
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(a.tmem_cols)
@@ -1247,7 +1252,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
       uint32_t need = 0;
       for (int q = 0; q < 4; ++q) {
         uint32_t c = 0;
-        for (int w = q; w < kConsumerWarps; w += 4) c += 4 * g.sched.warp_info[w * 3 + 0];
+        for (int w = q; w < static_cast<int>(g.sched.nconsumer); w += 4) c += 4 * g.sched.warp_info[w * 3 + 0];
         need = std::max(need, c);
       }
       uint32_t cols = 32;
@@ -1260,6 +1265,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
       a.tmem_cols = cols;
     }
     a.cont_base = g.sched.cont_base;
+    a.nc = g.sched.nconsumer;
     {
       // FSB_DEBUG experiments (1 = no TMA loads: wrong bytes by design; 2 = wait counters) exist
       // only in experiment builds (-DFSB_EXPERIMENTS); a release build never reads the variable

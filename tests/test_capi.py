@@ -347,3 +347,22 @@ def test_per_file_streams_reject_non_divisor():
         fsb.Graph.create(c, host_only=True)
     with pytest.raises(ValueError):
         oracle.generate_graph(c)
+
+
+@pytest.mark.parametrize("pw", ["5", "7"])
+def test_smem_schedule_with_more_precode_warps(pw):
+    """FSB_PRECODE_WARPS (read once per process, so a fresh pytest process): the schedule is dealt
+    over 27 - pw consumer warps and still covers every edge exactly once under the bank rule."""
+    import os
+    import subprocess
+    import sys as _sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FSB_PRECODE_WARPS=pw)
+    r = subprocess.run([_sys.executable, "-m", "pytest", "-q", "-m", "not gpu",
+                        os.path.join(root, "tests", "test_capi.py") + "::test_smem_schedule_covers_every_edge"],
+                       capture_output=True, text=True, env=env, timeout=600, cwd=root)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    code = ("from paper_1702_07409_b200 import configs, fsb; "
+            "g = fsb.Graph.create(configs.get(6), host_only=True); print(g.schedule()[2].shape[0])")
+    r = subprocess.run([_sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300, cwd=root)
+    assert r.returncode == 0 and int(r.stdout.strip()) == 27 - int(pw), r.stdout + r.stderr
