@@ -362,7 +362,7 @@ void build_smem_schedule(Graph &g) {
   s.tile_rows = s.zero_even + 2;
   s.data_units = s.kpad / kUnitRows;
   s.tile_units = (s.tile_rows + kUnitRows - 1) / kUnitRows;
-  if (g.prm.t % kSliceBytes != 0 || n > kMaxSmemRows || s.tile_rows > kMaxSmemSlots) return;
+  if (g.prm.t % kSliceBytes != 0 || g.prm.t > 0xFFFFFFFFull || n > kMaxSmemRows || s.tile_rows > kMaxSmemSlots) return;
   const uint16_t z0 = static_cast<uint16_t>(s.zero_even), z1 = static_cast<uint16_t>(s.zero_even + 1);
   auto slot = [&](int32_t m) -> uint16_t {
     const uint32_t r = static_cast<uint32_t>(m) < k ? static_cast<uint32_t>(m) : s.kpad + (m - k);

@@ -209,8 +209,14 @@ __device__ __forceinline__ void gather_xor_n(uint4 &acc, const uint4 &c, uint32_
 //     half-group's schedule, so half-group h holds row R_{h^1}): each row leaves as one full 128-B
 //     line -- the first tile's half from TMEM (the lane's own row) next to the partner's second
 //     half -- two stores per item.
-__device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t sbase, uint8_t *out, uint64_t t,
-                                        uint32_t half_id, uint32_t tcol, int kMode, uint32_t first) {
+// base + row * t in one IMAD.WIDE.U32 (row, t < 2^32)
+__device__ __forceinline__ uint8_t *row_addr(uint8_t *base, uint32_t row, uint32_t t) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(row), "r"(t), "l"(reinterpret_cast<uint64_t>(base)));
+  return reinterpret_cast<uint8_t *>(r);
+}
+__device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t sbase, uint8_t *out1, uint8_t *out2,
+                                        uint32_t t, uint32_t half_id, uint32_t tcol, int kMode) {
   const uint32_t row = h.x & 0xFFFFu;
   const uint32_t ctrl = h.x >> 16;
   const uint32_t L = ctrl & kMaxItemLen;
@@ -250,9 +256,9 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
   }
   if (kMode == 0) {
     if (wsplit) {
-      if (half_id == 0) st_stream(out + static_cast<uint64_t>(row) * t, acc);
+      if (half_id == 0) st_stream(row_addr(out1, row, t), acc);
     } else if (row != kNoRow) {
-      st_stream(out + static_cast<uint64_t>(row) * t, acc);
+      st_stream(row_addr(out1, row, t), acc);
     }
   } else if (kMode == 1) {
     tmem_st16(tcol, acc);
@@ -261,14 +267,13 @@ __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t s
     const uint32_t own = __shfl_xor_sync(0xffffffffu, row, 4);            // R_h (row = R_{h^1})
     const bool hi = half_id & 1;
     const uint32_t ra = hi ? row : own, rb = hi ? own : row;              // R_{2q}, R_{2q+1}
-    // `first` = byte offset in the line of the pair's first tile (0: slice s first, 64: s+1 first)
-    const uint32_t second = kSliceBytes - first;
+    // out1 / out2 = this lane's 16 B in the pair's line at the half it writes of R_{2q} / R_{2q+1}
+    // (per tile: even half-groups the first tile's half of R_{2q}, odd ones the second's, and the
+    // other way round for R_{2q+1})
     // line of R_{2q}: even half-group its first-tile half (TMEM), odd half-group the second (computed)
-    if (ra != kNoRow && (!wsplit || half_id < 2))
-      st_stream(out + static_cast<uint64_t>(ra) * t + (hi ? second : first), hi ? acc : prev);
+    if (ra != kNoRow && (!wsplit || half_id < 2)) st_stream(row_addr(out1, ra, t), hi ? acc : prev);
     // line of R_{2q+1}: even half-group the second-tile half (computed), odd half-group its first (TMEM)
-    if (rb != kNoRow && !wsplit)
-      st_stream(out + static_cast<uint64_t>(rb) * t + (hi ? first : second), hi ? prev : acc);
+    if (rb != kNoRow && !wsplit) st_stream(row_addr(out2, rb, t), hi ? prev : acc);
   }
 }
 
@@ -497,17 +502,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     else mbar_wait(smem_u32(&ready[b]), ph);  // FSB_WAIT_NS=0: hardware-suspended try_wait
     mbar_wait(smem_u32(&full[b]), ph);
     if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2], static_cast<unsigned long long>(clock64() - t_wait0));
-    // unpaired: this slice's 64 B; paired: the pair's 128-B line (slice s = the even one)
-    uint8_t *out = a.coded + stripe * a.coded_stride +
-                   static_cast<uint64_t>(mode ? (slice & ~1u) : slice) * kSliceBytes + lane4 * 16;
+    // unpaired: this slice's 64 B; paired: the pair's 128-B line (slice s = the even one), at the
+    // half this lane writes of R_{2q} (out1) and of R_{2q+1} (out2) -- `first` = byte offset in the
+    // line of the pair's first tile
+    uint8_t *out1 = a.coded + stripe * a.coded_stride +
+                    static_cast<uint64_t>(mode ? (slice & ~1u) : slice) * kSliceBytes + lane4 * 16;
+    uint8_t *out2 = out1;
+    if (mode) {
+      const bool hi = half_id & 1;
+      out1 += hi ? kSliceBytes - first : first;
+      out2 += hi ? first : kSliceBytes - first;
+    }
+    const uint32_t t32 = static_cast<uint32_t>(a.t);
     // items, with the next head chunk in flight (2-way unrolled so no register moves)
     for (uint32_t it = 0; it < nitems; it += 2) {
       const uint4 h1 = lds128(hp + kChunkBytes);
-      lt_item(h0, cp, sbase, out, a.t, half_id, tcol0 + 4 * it, mode, first);
+      lt_item(h0, cp, sbase, out1, out2, t32, half_id, tcol0 + 4 * it, mode);
       if (it + 1 >= nitems) break;
       h0 = lds128(hp + 2 * kChunkBytes);
       hp += 2 * kChunkBytes;
-      lt_item(h1, cp, sbase, out, a.t, half_id, tcol0 + 4 * (it + 1), mode, first);
+      lt_item(h1, cp, sbase, out1, out2, t32, half_id, tcol0 + 4 * (it + 1), mode);
     }
     if (mode == 1) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // parked before reuse
     __syncwarp();
