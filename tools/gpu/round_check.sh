@@ -8,7 +8,7 @@ mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
 nproc > $OUT/host.txt; lscpu | grep -E 'Model name|^CPU\(s\)|Thread' >> $OUT/host.txt
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo BUILD FAILED; tail -30 $OUT/build.log; exit 1; }
-timeout 900 python -m pytest tests -q -m gpu -x > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 1800 python -m pytest tests -q -m gpu -x > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 tail -3 $OUT/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 tail -2 $OUT/smoke.log
@@ -29,3 +29,10 @@ for op in decode repair update; do
 done
 python tools/gpu/partition_share.py 5 200 > $OUT/partition_share.json 2>&1
 python tools/gpu/stripe_share.py 300 > $OUT/stripe_share.json 2>&1; cat $OUT/stripe_share.json
+# config 5 (GLOBAL path): launch list + one full capture of the LT kernel
+C5="python bench.py --config 5 --steps 3 --warmup 3 --no-cpu --e2e-steps 0"
+$C5 > $OUT/plain_c5.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" -c 400 --csv --log-file $OUT/launches_c5.csv $C5 > $OUT/ncu_launches_c5.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:fsb_lt -s 3 -c 1 -o $OUT/prof_c5 $C5 > $OUT/ncu_full_c5.log 2>&1
+echo "ncu c5 rc=$?"
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench_reference.json 2> $OUT/bench_reference.err; tail -c 400 $OUT/bench_reference.json
