@@ -615,3 +615,18 @@ def test_window_kernel_shapes(regs, rows):
                        capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip().endswith("ok"), r.stdout
+
+
+@pytest.mark.parametrize("t,S", [(1040, 3), (528, 2), (2048, 5)])
+def test_window_kernel_multi_stripe_ragged(t, S):
+    """fsb_lt_win across stripes (unit = stripe x band x window) and with a ragged last band (t not a
+    multiple of 512: lanes past the end load a valid address and store nothing): config 3's code
+    (Omega, max degree 66, so windows exist) at other symbol sizes, every stripe against the oracle."""
+    _need_gpu()
+    cfg = dict(configs.get(3), t=t, stripes=S, k=2000, p=40, n=2400)
+    g = fsb.Graph.create(cfg)
+    assert g.info()["lt_windows"] > 0
+    D, C, Y = _oracle_case(cfg, S)
+    _, c, y = _run(cfg, fsb.VARIANT_GLOBAL, S=S)
+    _assert_equal(c, C, "checks t=%d S=%d" % (t, S))
+    _assert_equal(y, Y, "coded t=%d S=%d" % (t, S))
