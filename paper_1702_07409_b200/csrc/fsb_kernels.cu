@@ -1294,7 +1294,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
 #endif
       static const uint32_t wns = [] {
         const char *e = std::getenv("FSB_WAIT_NS");
-        return e ? static_cast<uint32_t>(std::atoi(e)) : 500u;
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
       }();
       a.wait_ns = wns;
     }
