@@ -136,6 +136,7 @@ def _dist_env():
 
 
 L2_BYTES = 126 * 1024 * 1024
+COLL_DEV = "cpu"  # device of the bench's collectives (set in main: the rank's GPU under NCCL)
 
 
 def plan(cfg, ws, rank, scaling, partition="rows"):
@@ -323,16 +324,26 @@ def main():
         return
 
     ws, rank, local = _dist_env()
+    # one GPU per rank; FSB_BENCH_BACKEND=gloo (host collectives, ranks may share a GPU: local %
+    # device count) exists only to exercise the N > 1 code path on a one-GPU box -- its timings
+    # are not bench values
+    backend = os.environ.get("FSB_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    global COLL_DEV
+    COLL_DEV = dev if backend == "nccl" else "cpu"
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         dist.barrier()
         t_bc = time.perf_counter()
-        g = fdist.broadcast_graph(cfg, device=dev)        # step a2 over NCCL
+        g = fdist.broadcast_graph(cfg, device=COLL_DEV)   # step a2 over NCCL
         torch.cuda.synchronize()
-        bcast_ms = fdist.max_over_ranks(1e3 * (time.perf_counter() - t_bc), device=dev)
+        bcast_ms = fdist.max_over_ranks(1e3 * (time.perf_counter() - t_bc), device=COLL_DEV)
     else:
         g = fsb.Graph.create(cfg)
     if args.variant != "auto":
@@ -404,7 +415,7 @@ def main():
     else:
         my_ms = evs[0].elapsed_time(evs[-1])
         per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
-    total_ms = fdist.max_over_ranks(my_ms, device=dev) if ws > 1 else my_ms
+    total_ms = fdist.max_over_ranks(my_ms, device=COLL_DEV) if ws > 1 else my_ms
     ms_per_step = total_ms / args.steps
     if kind == "stripes":
         src_bytes_all = (ws * S if args.scaling == "weak" else cfg["stripes"]) * k * t
@@ -455,7 +466,9 @@ def main():
         collectives = {"graph_broadcast_ms": round(bcast_ms, 3),
                        "graph_broadcast": "rank 0 generates, NCCL broadcast of the CSR, every rank "
                                           "rebuilds its schedule; host wall clock, max over ranks"}
-        if kind == "stripes" and args.scaling == "strong":
+        if kind == "stripes" and args.scaling == "strong" and COLL_DEV == "cpu":
+            collectives["result_gather"] = {"skipped": "FSB_BENCH_BACKEND=gloo test run (no P2P of device tensors)"}
+        elif kind == "stripes" and args.scaling == "strong":
             try:
                 collectives["result_gather"] = _time_gather(cod, cfg["stripes"], dev, ws)
             except Exception as e:  # reported, never fatal to the encode line
@@ -675,7 +688,7 @@ def _time_gather(cod, total, dev, ws, reps=3):
         out = fdist.gather_stripes(cod, total)
         b.record()
         torch.cuda.synchronize()
-        ms.append(fdist.max_over_ranks(a.elapsed_time(b), device=dev))
+        ms.append(fdist.max_over_ranks(a.elapsed_time(b), device=COLL_DEV))
         del out
     moved = (total - fdist.shard(total, ws, 0)[1]) * cod[0].numel()
     best = min(ms)
@@ -732,7 +745,7 @@ def _e2e_host(g, cfg, data, cod, S, args, dev, ws, src_bytes_all):
     e1.record(cur)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    ms = (fdist.max_over_ranks(ms, device=dev) if ws > 1 else ms) / args.e2e_steps
+    ms = (fdist.max_over_ranks(ms, device=COLL_DEV) if ws > 1 else ms) / args.e2e_steps
     ok = bool(torch.equal(h_cod[0].to(dev), cod[0]) and torch.equal(h_cod[S - 1].to(dev), cod[S - 1]))
     return {"value": round(src_bytes_all / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": S * k * t, "d2h_bytes_per_step": S * (p + n) * t,
@@ -789,7 +802,7 @@ def _e2e(g, cfg, data, cod, S, args, dev, ws, src_bytes_all):
     e1.record(cur)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    ms = (fdist.max_over_ranks(ms, device=dev) if ws > 1 else ms) / args.e2e_steps
+    ms = (fdist.max_over_ranks(ms, device=COLL_DEV) if ws > 1 else ms) / args.e2e_steps
     # spot-check the host result against the device-resident run
     ok = bool(torch.equal(h_cod[0].to(dev), cod[0]) and torch.equal(h_cod[S - 1].to(dev), cod[S - 1]))
     return {"value": round(src_bytes_all / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
