@@ -124,7 +124,23 @@ __device__ __forceinline__ uint4 tmem_ld16(uint32_t taddr) {
 // ============================================================================ SMEM kernel
 // Profiling experiments only (FSB_DEBUG=2): per consumer warp, cycles spent waiting for a tile
 // (ready/full barriers) and total cycles, summed over CTAs (read with fs_debug_counters).
-__device__ unsigned long long g_debug_counters[2 * 32];
+#ifdef FSB_EXPERIMENTS
+// FSB_DEBUG bit 4 (experiment builds, tools/gpu/timeline.py): per-CTA %globaltimer stamps from
+// index 64, 16 per CTA (entry, prologue done, first tile ready, mean / last consumer end, last TMA
+// issue, %smid, tiles, TMEM allocated, schedule staged, TMA thread past griddepcontrol.wait,
+// before / after the prologue barrier)
+constexpr uint32_t kDebugCounters = 64 + 16 * 256;
+#define FSB_TL(stmt) stmt
+#else
+constexpr uint32_t kDebugCounters = 64;
+#define FSB_TL(stmt)
+#endif
+__device__ unsigned long long g_debug_counters[kDebugCounters];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 struct SmemArgs {
   const uint4 *sched;          // heads ++ conts chunk streams (fsb_internal.h: SmemSchedule)
   const uint32_t *warp_info;   // nc x {items, head_off, cont_off}
@@ -337,11 +353,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 6);  // TMEM base address (paired mode)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t smem_base = smem_u32(smem);
+  FSB_TL(unsigned long long *tl = g_debug_counters + 64 + 16 * (blockIdx.x & 255);)
+  FSB_TL(if ((a.debug & 4) && threadIdx.x == 0) {
+    tl[0] = gtime();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    tl[6] = smid;
+  })
   if (a.paired && warp == 0) {  // one warp allocates the CTA's TMEM columns (one CTA per SM)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(a.tmem_cols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    FSB_TL(if ((a.debug & 4) && lane == 0) tl[8] = gtime();)
   }
 
   const int nc = static_cast<int>(a.nc);
@@ -358,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    FSB_TL(if (a.debug & 4) tl[10] = gtime();)
     uint32_t stripe, slice;
     if (tile_of(a, 0, stripe, slice)) {  // buffer 0 is free: no wait on `empty`
       if (a.debug & 1) {
@@ -387,18 +412,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  FSB_TL(if ((a.debug & 4) && threadIdx.x == 0) tl[9] = gtime();)
   for (uint32_t x = threadIdx.x; x < pre_n; x += blockDim.x) pre_s[x] = __ldg(&a.pre_slots[x]);
   if (threadIdx.x < 2 * 2 * (kSliceBytes / 16)) {  // 2 buffers x 2 rows x 4 lanes
     const uint32_t b = threadIdx.x >> 3, r = (threadIdx.x >> 2) & 1, l4 = threadIdx.x & 3;
     sts128(smem_base + b * buf_bytes + (a.zero_even + r) * kSliceBytes + l4 * 16, make_uint4(0, 0, 0, 0));
   }
+  FSB_TL(if ((a.debug & 4) && threadIdx.x == 0) tl[12] = gtime();)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  FSB_TL(if ((a.debug & 4) && threadIdx.x == 0) tl[13] = gtime();)
   // every thread past this point reads or writes user buffers after the previous grid is done;
   // the next launch may then start its prologue on SMs as they free up
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  FSB_TL(if ((a.debug & 4) && threadIdx.x == 0) tl[1] = gtime();)
 
   if (warp == nc) {
     // ---------------------------------------------------------------- TMA warp (one lane)
@@ -419,6 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_3d(buf + u * kUnitBytes, &tmap, smem_u32(&full[b]), static_cast<int32_t>(slice * kSliceBytes),
                       static_cast<int32_t>(u * kUnitRows), static_cast<int32_t>(stripe));
       }
+      FSB_TL(if (a.debug & 4) tl[5] = gtime();)
     }
     return;
   }
@@ -502,6 +532,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     else mbar_wait(smem_u32(&ready[b]), ph);  // FSB_WAIT_NS=0: hardware-suspended try_wait
     mbar_wait(smem_u32(&full[b]), ph);
     if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2], static_cast<unsigned long long>(clock64() - t_wait0));
+    FSB_TL(if ((a.debug & 4) && i == 0 && threadIdx.x == 0) tl[2] = gtime();)
+    FSB_TL(if ((a.debug & 4) && threadIdx.x == 0) tl[7] = i + 1;)
     // unpaired: this slice's 64 B; paired: the pair's 128-B line (slice s = the even one), at the
     // half this lane writes of R_{2q} (out1) and of R_{2q+1} (out2) -- `first` = byte offset in the
     // line of the pair's first tile
@@ -528,6 +560,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) mbar_arrive(smem_u32(&empty[b]));
   }
   if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2 + 1], static_cast<unsigned long long>(clock64() - t_start));
+  FSB_TL(if ((a.debug & 4) && lane == 0) {
+    const unsigned long long te = gtime();
+    atomicAdd(&tl[3], te / a.nc);
+    atomicMax(&tl[4], te);
+  })
   if (a.paired) {  // all consumer warps are done with TMEM; warp 0 frees it
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     consumer_bar(a.nc);
@@ -1660,11 +1697,11 @@ static fs_status launch_levels(const DecodePlan &pl, uint32_t S, uint8_t *coded,
 }
 
 fs_status read_debug_counters(uint64_t *out, uint32_t n) {
-  unsigned long long buf[64] = {0};
+  static unsigned long long buf[kDebugCounters];
   cudaError_t e = cudaMemcpyFromSymbol(buf, g_debug_counters, sizeof(buf));
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyFromSymbol");
-  for (uint32_t i = 0; i < n && i < 64; ++i) out[i] = buf[i];
-  const unsigned long long zero[64] = {0};
+  for (uint32_t i = 0; i < n && i < kDebugCounters; ++i) out[i] = buf[i];
+  static const unsigned long long zero[kDebugCounters] = {0};
   e = cudaMemcpyToSymbol(g_debug_counters, zero, sizeof(zero));
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
   return FS_OK;

@@ -1,0 +1,160 @@
+// Where can the SMEM kernel's per-tile schedule come from without using the shared-memory port?
+// 24 warps gather parity-paired 64-B rows from shared memory (8 half-groups x 4 lanes x 16 B per
+// LDS.128, as fsb_smem_encode does) for steps of a schedule that is identical every "tile":
+//   0: addresses from an in-register LCG (no schedule: the port's gather-only rate, mb8 variant 0)
+//   1: schedule in shared memory, one LDS.128 per lane per 8 steps (the half-group's 16-B chunk of
+//      8 slots, 16 bits each) -- today's design
+//   2: schedule in __constant__ memory, transposed: one warp-uniform 16-B word per step holding the
+//      8 half-groups' slots; each lane extracts its own 16 bits (no shared-memory traffic)
+//   3: as 2, but one uniform 16-B word per 2 steps for 4 half-group pairs... (8-bit deltas: skipped)
+//   4: schedule in global memory (L1-resident after the first tile), one LDG.128 per lane per 8 steps
+// Prints clk per warp-gather per SM.
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+constexpr int kRows = 1024;         // tile rows of 64 B
+constexpr int kWarps = 24;
+constexpr int kStepsPerWarp = 112;  // ~ config 4: 14,048 slots / 8 / 24 = 73 (+ heads); 112 for 16 chunks
+constexpr int kSchedWords = kWarps * kStepsPerWarp;  // 16-B words: 43 KB
+
+__constant__ uint4 c_sched[kSchedWords];
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void xr(uint4 &a, const uint4 &b) { a.x ^= b.x; a.y ^= b.y; a.z ^= b.z; a.w ^= b.w; }
+__device__ __forceinline__ uint32_t sel16(const uint4 &c, int i) {
+  const uint32_t w = (i >> 1) == 0 ? c.x : (i >> 1) == 1 ? c.y : (i >> 1) == 2 ? c.z : c.w;
+  return (i & 1) ? (w >> 16) : (w & 0xFFFFu);
+}
+
+template <int V>
+__global__ void __launch_bounds__(kWarps * 32, 1) k(const uint4 *g_sched_chunks, uint4 *out, int iters) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const uint32_t rows_b = sb, sched_b = sb + kRows * 64;
+  for (int i = threadIdx.x; i < kRows * 4; i += blockDim.x)
+    reinterpret_cast<uint4 *>(smem)[i] = make_uint4(i, i * 3, i * 7, i * 11);
+  for (int i = threadIdx.x; i < kSchedWords; i += blockDim.x)
+    reinterpret_cast<uint4 *>(smem + kRows * 64)[i] = g_sched_chunks[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, hg = lane >> 2, l4 = lane & 3;
+  const uint32_t lb = rows_b + l4 * 16;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  uint32_t h = (blockIdx.x * 4096 + (threadIdx.x >> 3)) * 2654435761u;
+  for (int it = 0; it < iters; ++it) {
+    if (V == 0) {
+      for (int s = 0; s < kStepsPerWarp; s += 8) {
+        uint4 x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          h = h * 1664525u + 1013904223u;
+          uint32_t ra = (h >> 8) & (kRows - 1), rb = (h >> 20) & (kRows - 1);
+          uint32_t r = (hg & 1) ? (rb | 1) : (ra & ~1u);
+          x[u] = lds128(lb + r * 64);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xr(acc, x[u]);
+      }
+    } else if (V == 1 || V == 4) {
+      // chunk j of this warp: 8 half-groups x 16 B, half-group hg's 8 slots for steps 8j..8j+7
+      const uint4 *gp = g_sched_chunks + warp * kStepsPerWarp + hg;
+      uint32_t cp = sched_b + (warp * kStepsPerWarp + hg) * 16;
+      uint4 c = (V == 1) ? lds128(cp) : __ldg(gp);
+      for (int s = 0; s < kStepsPerWarp; s += 8) {
+        cp += 128; gp += 8;
+        uint4 nx;
+        if (s + 8 < kStepsPerWarp) nx = (V == 1) ? lds128(cp) : __ldg(gp);
+        uint4 x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = lds128(lb + sel16(c, u) * 64);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xr(acc, x[u]);
+        c = nx;
+      }
+    } else if (V == 3) {
+      // one 32-bit constant load per lane and step: 4 distinct addresses per warp (half-group pairs)
+      uint32_t cbase;
+      asm("mov.u32 %0, c_sched;" : "=r"(cbase));
+      cbase += warp * kStepsPerWarp * 16 + (hg >> 1) * 4;
+      const int sh = (hg & 1) * 16;
+      for (int s = 0; s < kStepsPerWarp; s += 8) {
+        uint4 x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint32_t ww;
+          asm volatile("ld.const.u32 %0, [%1];" : "=r"(ww) : "r"(cbase + (s + u) * 16));
+          x[u] = lds128(lb + ((ww >> sh) & 0xFFFFu) * 64);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xr(acc, x[u]);
+      }
+    } else if (V == 2) {
+      const uint4 *cs = c_sched + warp * kStepsPerWarp;
+      const int sh = (hg & 1) * 16;
+      for (int s = 0; s < kStepsPerWarp; s += 8) {
+        uint4 x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint4 w = cs[s + u];  // warp-uniform: the 8 half-groups' slots of step s+u
+          const uint32_t ww = (hg >> 1) == 0 ? w.x : (hg >> 1) == 1 ? w.y : (hg >> 1) == 2 ? w.z : w.w;
+          x[u] = lds128(lb + ((ww >> sh) & 0xFFFFu) * 64);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xr(acc, x[u]);
+      }
+    }
+  }
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+template <int V>
+void run(const uint4 *gs, uint4 *out, int sms) {
+  const int iters = 2000;
+  const size_t smem = kRows * 64 + kSchedWords * 16;
+  cudaFuncSetAttribute(k<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<V><<<sms, kWarps * 32, smem>>>(gs, out, 4);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { printf("variant %d: %s\n", V, cudaGetErrorString(e)); return; }
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k<V><<<sms, kWarps * 32, smem>>>(gs, out, iters);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  const double gathers = (double)kWarps * iters * kStepsPerWarp;
+  printf("{\"variant\":%d,\"ms\":%.4f,\"clk_per_gather_per_sm\":%.3f}\n", V, ms, ms * 1e-3 * clk * 1e3 / gathers);
+}
+
+int main() {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  // slots: step s of warp w, half-group h: a random row of parity h & 1
+  std::vector<uint16_t> slot(kWarps * kStepsPerWarp * 8);
+  uint32_t x = 12345;
+  for (auto &v : slot) { x = x * 1664525u + 1013904223u; v = (x >> 12) & (kRows - 1); }
+  for (int w = 0; w < kWarps; ++w)
+    for (int s = 0; s < kStepsPerWarp; ++s)
+      for (int hh = 0; hh < 8; ++hh) {
+        uint16_t &v = slot[(w * kStepsPerWarp + s) * 8 + hh];
+        v = (hh & 1) ? (v | 1) : (v & ~1);
+      }
+  // transposed (per step, 8 half-groups) for __constant__; chunked (per half-group, 8 steps) for smem
+  std::vector<uint16_t> tr(slot), ch(slot.size());
+  for (int w = 0; w < kWarps; ++w)
+    for (int j = 0; j < kStepsPerWarp / 8; ++j)
+      for (int hh = 0; hh < 8; ++hh)
+        for (int u = 0; u < 8; ++u)
+          ch[((w * kStepsPerWarp * 8) + j * 64 + hh * 8 + u)] = slot[(w * kStepsPerWarp + j * 8 + u) * 8 + hh];
+  cudaMemcpyToSymbol(c_sched, tr.data(), tr.size() * 2);
+  uint4 *gs; cudaMalloc(&gs, ch.size() * 2);
+  cudaMemcpy(gs, ch.data(), ch.size() * 2, cudaMemcpyHostToDevice);
+  uint4 *out; cudaMalloc(&out, 1 << 24);
+  for (int r = 0; r < 2; ++r) { run<0>(gs, out, sms); run<1>(gs, out, sms); run<2>(gs, out, sms); run<3>(gs, out, sms); run<4>(gs, out, sms); }
+  return 0;
+}
