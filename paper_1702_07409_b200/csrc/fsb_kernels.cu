@@ -129,11 +129,16 @@ __device__ __forceinline__ uint4 tmem_ld16(uint32_t taddr) {
 // index 64, 16 per CTA (entry, prologue done, first tile ready, mean / last consumer end, last TMA
 // issue, %smid, tiles, TMEM allocated, schedule staged, TMA thread past griddepcontrol.wait,
 // before / after the prologue barrier)
-constexpr uint32_t kDebugCounters = 64 + 16 * 256;
+constexpr uint32_t kDebugCounters = 64 + 16 * 256 + 2 * 128 * 8;
+// FSB_DEBUG bit 8: per-tile log of CTAs 0 and gridDim/2 from index 64 + 16*256, 8 per tile (tiles
+// < 128): TMA issue done, full seen, ready arrived, consumer start min / max, end min / max
+// (min stored as ~t so atomicMax keeps it)
+#define FSB_TLOG(stmt) stmt
 #define FSB_TL(stmt) stmt
 #else
 constexpr uint32_t kDebugCounters = 64;
 #define FSB_TL(stmt)
+#define FSB_TLOG(stmt)
 #endif
 __device__ unsigned long long g_debug_counters[kDebugCounters];
 __device__ __forceinline__ unsigned long long gtime() {
@@ -354,6 +359,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t smem_base = smem_u32(smem);
   FSB_TL(unsigned long long *tl = g_debug_counters + 64 + 16 * (blockIdx.x & 255);)
+  FSB_TLOG(unsigned long long *tlog = (a.debug & 8) && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2)
+                                          ? g_debug_counters + 64 + 16 * 256 + (blockIdx.x ? 128 * 8 : 0)
+                                          : nullptr;)
   FSB_TL(if ((a.debug & 4) && threadIdx.x == 0) {
     tl[0] = gtime();
     uint32_t smid;
@@ -393,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_3d(smem_base + u * kUnitBytes, &tmap, smem_u32(&full[0]), static_cast<int32_t>(slice * kSliceBytes),
                       static_cast<int32_t>(u * kUnitRows), static_cast<int32_t>(stripe));
       }
+      FSB_TLOG(if (tlog) tlog[0] = gtime();)
     }
   }
   // the schedule (identical for every tile) and the two zero rows of each buffer
@@ -447,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t u = 0; u < a.data_units && !(a.debug & 1); ++u)
           tma_load_3d(buf + u * kUnitBytes, &tmap, smem_u32(&full[b]), static_cast<int32_t>(slice * kSliceBytes),
                       static_cast<int32_t>(u * kUnitRows), static_cast<int32_t>(stripe));
+        FSB_TLOG(if (tlog && i < 128) tlog[i * 8 + 0] = gtime();)
       }
       FSB_TL(if (a.debug & 4) tl[5] = gtime();)
     }
@@ -468,6 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(smem_u32(&full[b]), ph);
       if ((a.debug & 2) && lane == 0)
         atomicAdd(&g_debug_counters[48 + 2 * pw], static_cast<unsigned long long>(clock64() - tw0));
+      FSB_TLOG(if (tlog && i < 128 && pw == 0 && lane == 0) tlog[i * 8 + 1] = gtime();)
       // precode, level by level (a check may read checks of earlier levels, Alg 2): check c of
       // a level by half-group (c - level start) % 8, 16 B per lane
       const uint32_t lb = buf + lane4 * 16;
@@ -495,6 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // this level's check rows before the next level reads them (all precode warps)
         asm volatile("bar.sync 2, %0;" ::"r"(npw * 32) : "memory");
       }
+      FSB_TLOG(if (tlog && i < 128 && pw == 0 && lane == 0) tlog[i * 8 + 2] = gtime();)
       if (pw == 0 && lane == 0) mbar_arrive(smem_u32(&ready[b]));  // release: data + checks visible
     }
     if ((a.debug & 2) && lane == 0)
@@ -534,6 +546,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2], static_cast<unsigned long long>(clock64() - t_wait0));
     FSB_TL(if ((a.debug & 4) && i == 0 && threadIdx.x == 0) tl[2] = gtime();)
     FSB_TL(if ((a.debug & 4) && threadIdx.x == 0) tl[7] = i + 1;)
+    FSB_TLOG(if (tlog && i < 128 && lane == 0) {
+      const unsigned long long tn = gtime();
+      atomicMax(&tlog[i * 8 + 3], ~tn);
+      atomicMax(&tlog[i * 8 + 4], tn);
+    })
     // unpaired: this slice's 64 B; paired: the pair's 128-B line (slice s = the even one), at the
     // half this lane writes of R_{2q} (out1) and of R_{2q+1} (out2) -- `first` = byte offset in the
     // line of the pair's first tile
@@ -557,6 +574,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (mode == 1) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // parked before reuse
     __syncwarp();
+    FSB_TLOG(if (tlog && i < 128 && lane == 0) {
+      const unsigned long long tn = gtime();
+      atomicMax(&tlog[i * 8 + 5], ~tn);
+      atomicMax(&tlog[i * 8 + 6], tn);
+    })
     if (lane == 0) mbar_arrive(smem_u32(&empty[b]));
   }
   if ((a.debug & 2) && lane == 0) atomicAdd(&g_debug_counters[warp * 2 + 1], static_cast<unsigned long long>(clock64() - t_start));
