@@ -8,6 +8,10 @@
 //      8 half-groups' slots; each lane extracts its own 16 bits (no shared-memory traffic)
 //   3: as 2, but one uniform 16-B word per 2 steps for 4 half-group pairs... (8-bit deltas: skipped)
 //   4: schedule in global memory (L1-resident after the first tile), one LDG.128 per lane per 8 steps
+//   5: 32-B lanes ("quarter-groups" of 2 lanes per 64-B row, 16 per warp): per slot two LDS.128 per
+//      lane (pieces 2*l2+s and 2*l2+1-s, s = group & 1, so a phase's 8 lanes hit 8 bank quads when
+//      groups g and g^2 read rows of opposite parity); one schedule LDS.128 per lane per 8 slots
+//      feeds 16 gathers
 // Prints clk per warp-gather per SM.
 #include <cstdio>
 #include <cstdint>
@@ -76,6 +80,33 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k(const uint4 *g_sched_chunks,
         for (int u = 0; u < 8; ++u) xr(acc, x[u]);
         c = nx;
       }
+    } else if (V == 5) {
+      // 16 groups x 16 B per chunk (256 B); the group's 8 slots for 8 steps
+      const int qg = lane >> 1, l2 = lane & 1, sg = qg & 1;
+      const uint32_t la = rows_b + 32 * l2 + 16 * sg, lb2 = la ^ 16;
+      uint32_t cp = sched_b + (warp * kStepsPerWarp + qg) * 16;
+      uint4 c = lds128(cp);
+      uint4 acc2 = make_uint4(0, 0, 0, 0);
+      for (int s = 0; s < kStepsPerWarp; s += 16) {  // 8 slots = 16 gathers per chunk
+        cp += 256;
+        uint4 nx;
+        if (s + 16 < kStepsPerWarp) nx = lds128(cp);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint4 x[4], y[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint32_t r = sel16(c, hh * 4 + u);
+            r = (qg & 2) ? (r | 1) : (r & ~1u);  // groups g, g^2: opposite parities
+            x[u] = lds128(la + r * 64);
+            y[u] = lds128(lb2 + r * 64);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) { xr(acc, x[u]); xr(acc2, y[u]); }
+        }
+        c = nx;
+      }
+      xr(acc, acc2);
     } else if (V == 3) {
       // one 32-bit constant load per lane and step: 4 distinct addresses per warp (half-group pairs)
       uint32_t cbase;
@@ -155,6 +186,6 @@ int main() {
   uint4 *gs; cudaMalloc(&gs, ch.size() * 2);
   cudaMemcpy(gs, ch.data(), ch.size() * 2, cudaMemcpyHostToDevice);
   uint4 *out; cudaMalloc(&out, 1 << 24);
-  for (int r = 0; r < 2; ++r) { run<0>(gs, out, sms); run<1>(gs, out, sms); run<2>(gs, out, sms); run<3>(gs, out, sms); run<4>(gs, out, sms); }
+  for (int r = 0; r < 2; ++r) { run<0>(gs, out, sms); run<1>(gs, out, sms); run<2>(gs, out, sms); run<3>(gs, out, sms); run<4>(gs, out, sms); run<5>(gs, out, sms); }
   return 0;
 }
