@@ -332,14 +332,17 @@ fs_status build_precode_levels(Graph &g) {
 // Degree-aware, edge-balanced, bank-conflict-free split of one tile's LT work over
 // kConsumerWarps warps (record format and bank rule: fsb_internal.h).
 //
-// - Rows of degree > kSplitThreshold become split items: their even tile rows are dealt
-//   round-robin to the 4 half-0 half-groups and their odd rows to the 4 half-1 half-groups.
-// - Lighter rows are paired (A for half 0, B for half 1 of one group): within a degree class,
+// - Rows of degree in (kSplitThreshold, kSplit2Max] become pair-splits (evens in half 0, odds in
+//   half 1 of one pair of groups); heavier rows become warp-split items: their even tile rows are
+//   dealt round-robin to the 8 half-0 groups and their odd rows to the 8 half-1 groups.
+// - Lighter rows are paired (A for half 0, B for half 1 of one pair): within a degree class,
 //   rows are sorted by their number of even sources and the most-even row is paired with the
 //   least-even one, so that A's evens meet B's odds and A's odds meet B's evens; leftovers are
 //   matched with the zero row of the opposite parity.  Pairs are sorted by length and packed
-//   4 per item (the item length is the longest pair's; shorter pairs pad with zero rows).
-// - Items are dealt longest-first to the least loaded warp (LPT).
+//   8 per item (the item length is the longest pair's; shorter pairs pad with zero rows).
+// - Items are dealt longest-first to the least loaded warp (LPT), an item costing its length
+//   plus a per-item overhead (default 12 steps: same-box A/B of the 16-group items, config 4
+//   0.5826 -> 0.5741 ms against 6, 20 ties; profiles/r02_s4/ab_groups16.txt).
 void build_smem_schedule(Graph &g) {
   SmemSchedule &s = g.sched;
   s = SmemSchedule();
@@ -376,10 +379,11 @@ void build_smem_schedule(Graph &g) {
     std::vector<uint16_t> seq[2];    // seq[0][e] even <=> seq[1][e] odd
     bool split = false;              // pair-split: A and B hold the two parts of row[0]
   };
+  constexpr int kPairsPerItem = kGroupsPerWarp / 2;
   struct Item {
     bool split = false;
     uint32_t len = 0;
-    Pair grp[4];
+    Pair grp[kPairsPerItem];
   };
   auto row_slots = [&](uint32_t j, std::vector<uint16_t> &ev, std::vector<uint16_t> &od) {
     for (int32_t e = g.lt_row_ptr[j]; e < g.lt_row_ptr[j + 1]; ++e) {
@@ -412,12 +416,21 @@ void build_smem_schedule(Graph &g) {
     return pr;
   };
 
+  // split thresholds (FSB_SPLIT1 / FSB_SPLIT2 override kSplitThreshold / kSplit2Max: tuning)
+  static const uint32_t split1 = [] {
+    const char *e = std::getenv("FSB_SPLIT1");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : static_cast<uint32_t>(kSplitThreshold);
+  }();
+  static const uint32_t split2 = [] {
+    const char *e = std::getenv("FSB_SPLIT2");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : static_cast<uint32_t>(kSplit2Max);
+  }();
   std::vector<Item> items;
   std::vector<uint32_t> light;
   std::vector<Pair> pairs;
   for (uint32_t j = 0; j < n; ++j) {
     const uint32_t d = static_cast<uint32_t>(g.lt_row_ptr[j + 1] - g.lt_row_ptr[j]);
-    if (d > static_cast<uint32_t>(kSplitThreshold) && d <= static_cast<uint32_t>(kSplit2Max)) {
+    if (d > split1 && d <= split2) {
       // pair-split: evens in half 0, odds in half 1 of one group
       Pair pr;
       pr.split = true;
@@ -433,21 +446,21 @@ void build_smem_schedule(Graph &g) {
       pairs.push_back(std::move(pr));
       continue;
     }
-    if (d > static_cast<uint32_t>(kSplitThreshold)) {
+    if (d > split1) {
       Item it;
       it.split = true;
       std::vector<uint16_t> ev, od;
       row_slots(j, ev, od);
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kPairsPerItem; ++q) {
         it.grp[q].row[0] = it.grp[q].row[1] = static_cast<uint16_t>(j);
-        for (size_t e = q; e < ev.size(); e += 4) it.grp[q].seq[0].push_back(ev[e]);
-        for (size_t e = q; e < od.size(); e += 4) it.grp[q].seq[1].push_back(od[e]);
+        for (size_t e = q; e < ev.size(); e += kPairsPerItem) it.grp[q].seq[0].push_back(ev[e]);
+        for (size_t e = q; e < od.size(); e += kPairsPerItem) it.grp[q].seq[1].push_back(od[e]);
       }
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kPairsPerItem; ++q) {
         it.len = std::max<uint32_t>(it.len, static_cast<uint32_t>(
                                                 std::max(it.grp[q].seq[0].size(), it.grp[q].seq[1].size())));
       }
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kPairsPerItem; ++q) {
         it.grp[q].seq[0].resize(it.len, z0);
         it.grp[q].seq[1].resize(it.len, z1);
       }
@@ -513,13 +526,13 @@ void build_smem_schedule(Graph &g) {
   if (carry != UINT32_MAX) pairs.push_back(make_pair(carry, UINT32_MAX));
   std::stable_sort(pairs.begin(), pairs.end(),
                    [](const Pair &a, const Pair &b) { return a.seq[0].size() > b.seq[0].size(); });
-  for (size_t i = 0; i < pairs.size(); i += 4) {
+  for (size_t i = 0; i < pairs.size(); i += kPairsPerItem) {
     Item it;
-    for (int q = 0; q < 4 && i + q < pairs.size(); ++q) {
+    for (int q = 0; q < kPairsPerItem && i + q < pairs.size(); ++q) {
       it.grp[q] = pairs[i + q];
       it.len = std::max<uint32_t>(it.len, static_cast<uint32_t>(it.grp[q].seq[0].size()));
     }
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kPairsPerItem; ++q) {
       it.grp[q].seq[0].resize(it.len, z0);
       it.grp[q].seq[1].resize(it.len, z1);
     }
@@ -527,12 +540,11 @@ void build_smem_schedule(Graph &g) {
   }
   for (const Item &it : items)
     if (it.len > kMaxItemLen || it.len == 0) return;
-  // LPT over warps; cost ~ gather steps + per-item overhead (head, dispatch, store)
   // LPT cost of an item in gather steps: L plus a per-item overhead (head load, dispatch, store);
   // FSB_ITEM_OVERHEAD overrides it (tuning experiments)
   static const uint32_t overhead = [] {
     const char *e = std::getenv("FSB_ITEM_OVERHEAD");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 6u;
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 12u;
   }();
   auto cost = [](const Item &it) { return it.len + overhead + (it.split ? 2u : 0u); };
   std::vector<uint32_t> order(items.size());
@@ -555,12 +567,13 @@ void build_smem_schedule(Graph &g) {
   if (const char *dbg = std::getenv("FSB_SCHED_DEBUG")) {
     if (std::string(dbg) == "zero")
       for (Item &it : items)
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kPairsPerItem; ++q)
           for (int hh = 0; hh < 2; ++hh)
             for (uint16_t &v : it.grp[q].seq[hh]) v = hh ? z1 : z0;
   }
 #endif
-  // emit the two chunk streams, warp after warp (32 words per chunk; half-group h: words 4h..4h+3)
+  // emit the two chunk streams, warp after warp (64 words per chunk; group g: words 4g..4g+3;
+  // pair q, half hh in group 4(q>>1) + (q&1) + 2hh)
   s.warp_info.assign(ncw * 3, 0);
   std::vector<uint32_t> heads, conts;
   auto put = [](uint32_t &word, uint32_t i, uint16_t v) {  // slot i of a word pair position
@@ -576,16 +589,18 @@ void build_smem_schedule(Graph &g) {
     uint32_t steps = 0;
     for (uint32_t idx : per_warp[w]) {
       const Item &it = items[idx];
-      const bool item_pair_split = it.grp[0].split || it.grp[1].split || it.grp[2].split || it.grp[3].split;
+      bool item_pair_split = false;
+      for (int q = 0; q < kPairsPerItem; ++q) item_pair_split = item_pair_split || it.grp[q].split;
       const size_t hb = heads.size();
       heads.resize(hb + wpc, 0);
       const uint32_t ncont = it.len > kHeadSlots ? (it.len - kHeadSlots + kChunkSlots - 1) / kChunkSlots : 0;
       const size_t cb = conts.size();
       conts.resize(cb + static_cast<size_t>(ncont) * wpc, 0);
-      for (int h = 0; h < kHalvesPerWarp; ++h) {
-        const Pair &pr = it.grp[h >> 1];
-        const std::vector<uint16_t> &seq = pr.seq[h & 1];
-        heads[hb + h * 4] = static_cast<uint32_t>(pr.row[h & 1]) |
+      for (int h = 0; h < kGroupsPerWarp; ++h) {
+        const int q = ((h >> 2) << 1) | (h & 1), hh = (h >> 1) & 1;  // pair, half
+        const Pair &pr = it.grp[q];
+        const std::vector<uint16_t> &seq = pr.seq[hh];
+        heads[hb + h * 4] = static_cast<uint32_t>(pr.row[hh]) |
                             (static_cast<uint32_t>(it.len | (it.split ? kSplitBit : 0) |
                                                    (item_pair_split ? kPairSplitBit : 0))
                              << 16);
@@ -600,7 +615,7 @@ void build_smem_schedule(Graph &g) {
           }
         }
         // unused slot positions of the last chunk: parity-correct zero rows (never read)
-        const uint16_t zp = (h & 1) ? z1 : z0;
+        const uint16_t zp = hh ? z1 : z0;
         for (uint32_t e = it.len; e < kHeadSlots + ncont * kChunkSlots; ++e) {
           if (e < kHeadSlots) {
             put(heads[hb + h * 4 + 1 + e / 2], e, zp);

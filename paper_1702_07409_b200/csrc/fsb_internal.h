@@ -20,37 +20,45 @@ constexpr int kSliceBytes = 64;
 constexpr int kUnitRows = 64;
 constexpr int kUnitBytes = kUnitRows * kSliceBytes;     // 4 KiB
 constexpr int kConsumerWarps = 24;
-constexpr int kHalvesPerWarp = 8;                        // half-groups: 4 lanes x 16 B = 64 B
+constexpr int kHalvesPerWarp = 8;                        // precode half-groups: 4 lanes x 16 B = 64 B
+constexpr int kGroupsPerWarp = 16;                       // LT groups: 2 lanes x 32 B = 64 B
 constexpr int kPrecodeWarps = 3;                         // precode (a3) warps per CTA
 constexpr int kThreads = (kConsumerWarps + 1 + kPrecodeWarps) * 32;  // + 1 TMA warp
 constexpr int kSplitThreshold = 60;                      // rows of degree > this are split:
 constexpr int kSplit2Max = 120;                           //   over the 2 halves of a group (<= this)
                                                          //   or over the 8 half-groups of a warp
 
-// Bank rule: a 128-bit shared load is served in phases of 8 lanes = two half-groups (lanes
-// 8q..8q+3 = half 0, 8q+4..8q+7 = half 1).  A 64-B row r occupies the 16 banks of half (r & 1)
-// of a 128-B line, so the two rows one phase reads are conflict-free iff their parities
-// differ.  The host schedule guarantees it: in every step, half 0 of group q reads an even row
-// exactly when half 1 reads an odd row (padding uses the even / odd zero rows).
+// LT work is done by *groups* of 2 lanes, 16 per warp: group g = lanes 2g, 2g+1; lane l2 = lane & 1
+// owns the 32 contiguous bytes 32*l2 .. 32*l2+31 of a 64-B row slice and reads them with two
+// 128-bit shared loads per slot (pieces 2*l2+s and 2*l2+1-s, s = g & 1).
+// Bank rule: a 128-bit shared load is served in phases of 8 lanes = groups 4m..4m+3.  A 64-B row r
+// occupies the 16 banks of half (r & 1) of a 128-B line; the two groups of a phase with the same s
+// read two different 16-B pieces of their rows per load, so the phase is conflict-free iff groups
+// g and g^2 read rows of opposite parity (then the 8 lanes cover 8 distinct 16-B bank quads).  The
+// host schedule guarantees it in every step: a *pair* of rows sits in groups (g, g^2) -- pair q
+// in groups 4(q>>1) + (q&1) (half 0) and that + 2 (half 1) -- and half 0 reads an even row exactly
+// when half 1 reads an odd row (padding uses the even / odd zero rows).  Against 16-B lanes (4 per
+// row) one schedule load feeds twice the gathers and a warp's item carries 16 rows instead of 8
+// (tools/microbench/mb15.cu variant 5: 4.15 clk per gather vs 4.29).
 //
 // Item-record schedule.  A warp's per-tile LT work is a list of *items*; an item gives each of
-// the warp's 8 half-groups one output row and the same number L of source slots.  A slot is an
+// the warp's 16 groups one output row and the same number L of source slots.  A slot is an
 // 11-bit tile row (data m -> m, check i -> kpad+i, padding -> zero_even / zero_odd); two slots
 // share a 32-bit word as  a | b << 21  (bits 11..20 zero; bits 11..14 may carry flags, which the
 // address arithmetic ignores), so the kernel forms the shared address of `b` with one shift-add
-// (sbase + (w >> 15)).  Two streams, copied into shared memory once per CTA, in 128-byte chunks
-// (8 half-groups x 16 B; half-group g's 16 B at uint4 index chunk*8 + g):
+// (sbase + (w >> 15)).  Two streams, copied into shared memory once per CTA, in 256-byte chunks
+// (16 groups x 16 B; group g's 16 B at uint4 index chunk*16 + g):
 //   heads: one chunk per item: word 0 = row | ctrl << 16, words 1..3 = slots 0..5; ctrl =
-//          L | pair-split << 14 | warp-split << 15 (identical in all 8 half-groups); row =
-//          kNoRow for a half-group that stores nothing; word 1 bit 11 (kPairFlag) marks a
-//          half-group whose partner half holds the other part of the same row;
+//          L | pair-split << 14 | warp-split << 15 (identical in all 16 groups); row =
+//          kNoRow for a group that stores nothing; word 1 bit 11 (kPairFlag) marks a
+//          group whose partner half holds the other part of the same row;
 //   conts: slots 6.. of items with L > 6, 8 per chunk (4 words), items in the same order.
-// Heavy rows: degree <= kSplit2Max -> a pair-split: evens in half 0, odds in half 1 of one group
+// Heavy rows: degree <= kSplit2Max -> a pair-split: evens in half 0, odds in half 1 of one pair
 // (combined by one xor-4 warp shuffle, stored by half 0); larger -> a warp-split item: evens over
-// the four half-0, odds over the four half-1 half-groups (three warp shuffles, same row in all 8).
+// the eight half-0, odds over the eight half-1 groups (four warp shuffles, same row in all 16).
 constexpr uint32_t kHeadSlots = 6;          // slots in an item's head chunk
 constexpr uint32_t kChunkSlots = 8;         // slots in a continuation chunk
-constexpr uint32_t kChunkBytes = kHalvesPerWarp * 16;
+constexpr uint32_t kChunkBytes = kGroupsPerWarp * 16;
 constexpr uint32_t kStreamPad = 2;          // zero chunks after each stream (prefetch overrun)
 constexpr uint32_t kSlotBits = 11;
 constexpr uint32_t kSlotHiShift = 21;

@@ -103,6 +103,32 @@ __device__ __forceinline__ void xor_into(uint4 &a, const uint4 &b) {
 __device__ __forceinline__ void st_stream(uint8_t *p, const uint4 &v) {
   __stcs(reinterpret_cast<uint4 *>(p), v);
 }
+// 32 contiguous bytes (lo = the first 16): one 256-bit streaming store when the caller's coded
+// buffer is 32-B aligned (base and stride; warp-uniform), else two 128-bit ones
+__device__ __forceinline__ void st_stream32(uint8_t *p, const uint4 &lo, const uint4 &hi, bool st256) {
+  if (st256) {
+    asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(lo.x), "r"(lo.y),
+                 "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+                 : "memory");
+  } else {
+    st_stream(p, lo);
+    st_stream(p + 16, hi);
+  }
+}
+// 32 B per lane at 8 consecutive 32-bit columns of this warp's lane quarter
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint4 &lo, const uint4 &hi) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(lo.x), "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint4 &lo, uint4 &hi) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+      : "r"(taddr)
+      : "memory");
+}
 // Tensor memory (TMEM): 16 B per lane at 4 consecutive 32-bit columns of this warp's lane quarter.
 // tcgen05.ld/st do not use the L1TEX/LSU pipe the gathers saturate (tools/microbench/mb8.cu).
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint4 &v) {
@@ -196,40 +222,53 @@ __device__ __forceinline__ uint32_t slot_addr(const uint4 &c, int h, uint32_t sb
   return addr;
 }
 
-// acc ^= tile rows named by slots [H0, H0+N) of chunk c.  All N shared-memory loads are issued
-// before the XOR chain so they overlap.
+// accA / accB ^= the lane's two 16-B pieces of the tile rows named by slots [H0, H0+N) of chunk
+// c: piece at sbase + row*64 and the one at (that ^ 16) -- sbase carries 32*l2 + 16*(g & 1), so the
+// lane reads pieces 2*l2 + (g&1) and 2*l2 + 1 - (g&1) (bank rule, fsb_internal.h).  All 2N loads
+// are issued before the XOR chains so they overlap.
 template <int H0, int N>
-__device__ __forceinline__ void gather_xor(uint4 &acc, const uint4 &c, uint32_t sbase) {
-  uint4 x[N];
+__device__ __forceinline__ void gather2(uint4 &accA, uint4 &accB, const uint4 &c, uint32_t sbase) {
+  uint4 x[N], y[N];
 #pragma unroll
-  for (int i = 0; i < N; ++i) x[i] = lds128(slot_addr(c, H0 + i, sbase));
+  for (int i = 0; i < N; ++i) {
+    const uint32_t a = slot_addr(c, H0 + i, sbase);
+    x[i] = lds128(a);
+    y[i] = lds128(a ^ 16u);
+  }
 #pragma unroll
-  for (int i = 0; i < N; ++i) xor_into(acc, x[i]);
+  for (int i = 0; i < N; ++i) {
+    xor_into(accA, x[i]);
+    xor_into(accB, y[i]);
+  }
 }
 
+// slots [H0, H0 + n) of chunk c, 1 <= n <= min(4, 8 - H0)
 template <int H0>
-__device__ __forceinline__ void gather_xor_n(uint4 &acc, const uint4 &c, uint32_t n, uint32_t sbase) {
+__device__ __forceinline__ void gather2_n(uint4 &accA, uint4 &accB, const uint4 &c, uint32_t n, uint32_t sbase) {
   switch (n) {
-    case 1: gather_xor<H0, 1>(acc, c, sbase); break;
-    case 2: gather_xor<H0, 2>(acc, c, sbase); break;
-    case 3: gather_xor<H0, 3>(acc, c, sbase); break;
-    case 4: gather_xor<H0, 4>(acc, c, sbase); break;
-    case 5: if (H0 + 5 <= 8) gather_xor<H0, (H0 + 5 <= 8 ? 5 : 1)>(acc, c, sbase); break;
-    case 6: if (H0 + 6 <= 8) gather_xor<H0, (H0 + 6 <= 8 ? 6 : 1)>(acc, c, sbase); break;
-    case 7: if (H0 + 7 <= 8) gather_xor<H0, (H0 + 7 <= 8 ? 7 : 1)>(acc, c, sbase); break;
-    default: if (H0 == 0) gather_xor<H0, (H0 == 0 ? 8 : 1)>(acc, c, sbase); break;
+    case 1: gather2<H0, 1>(accA, accB, c, sbase); break;
+    case 2: gather2<H0, 2>(accA, accB, c, sbase); break;
+    case 3: if (H0 + 3 <= 8) gather2<H0, (H0 + 3 <= 8 ? 3 : 1)>(accA, accB, c, sbase); break;
+    default: if (H0 + 4 <= 8) gather2<H0, (H0 + 4 <= 8 ? 4 : 1)>(accA, accB, c, sbase); break;
   }
+}
+
+__device__ __forceinline__ void shfl_xor_into(uint4 &a, int o) {
+  a.x ^= __shfl_xor_sync(0xffffffffu, a.x, o);
+  a.y ^= __shfl_xor_sync(0xffffffffu, a.y, o);
+  a.z ^= __shfl_xor_sync(0xffffffffu, a.z, o);
+  a.w ^= __shfl_xor_sync(0xffffffffu, a.w, o);
 }
 
 // One item (fsb_internal.h): head chunk h, continuation chunks at *cp (shared address, advanced),
 // XOR in registers, then the row results leave according to kMode:
 // (kMode is warp-uniform and a runtime value: one inlined copy serves all three modes)
-//   0 (unpaired): one 64-B store per half-group (split items: combined over the halves);
-//   1 (paired, the pair's first tile): nothing leaves; each lane parks its 16 B in TMEM block `tcol`;
-//   2 (paired, second tile = the other 64-B half of the same 128-B lines, read with the partner
-//     half-group's schedule, so half-group h holds row R_{h^1}): each row leaves as one full 128-B
-//     line -- the first tile's half from TMEM (the lane's own row) next to the partner's second
-//     half -- two stores per item.
+//   0 (unpaired): one 64-B store per group (split items: combined over the halves);
+//   1 (paired, the pair's first tile): nothing leaves; each lane parks its 32 B in TMEM block `tcol`;
+//   2 (paired, second tile = the other 64-B half of the same 128-B lines, read with group g^1's
+//     schedule, so group g holds row R_{g^1}): each row leaves as one full 128-B line -- the first
+//     tile's half from TMEM (the lane's own row) next to the partner group's second half -- two
+//     256-bit stores per lane and item.
 // base + row * t in one IMAD.WIDE.U32 (row, t < 2^32)
 __device__ __forceinline__ uint8_t *row_addr(uint8_t *base, uint32_t row, uint32_t t) {
   uint64_t r;
@@ -237,64 +276,74 @@ __device__ __forceinline__ uint8_t *row_addr(uint8_t *base, uint32_t row, uint32
   return reinterpret_cast<uint8_t *>(r);
 }
 __device__ __forceinline__ void lt_item(const uint4 &h, uint32_t &cp, uint32_t sbase, uint8_t *out1, uint8_t *out2,
-                                        uint32_t t, uint32_t half_id, uint32_t tcol, int kMode) {
+                                        uint32_t t, uint32_t grp, uint32_t tcol, int kMode, bool st256) {
   const uint32_t row = h.x & 0xFFFFu;
   const uint32_t ctrl = h.x >> 16;
   const uint32_t L = ctrl & kMaxItemLen;
-  uint4 acc = make_uint4(0, 0, 0, 0);
+  uint4 accA = make_uint4(0, 0, 0, 0), accB = make_uint4(0, 0, 0, 0);
   // the first continuation chunk is requested before the head gathers, so its latency overlaps
   // them instead of following them
   uint4 c = make_uint4(0, 0, 0, 0);
   if (L > kHeadSlots) c = lds128(cp);
-  gather_xor_n<2>(acc, h, L < kHeadSlots ? L : kHeadSlots, sbase);
+  gather2_n<2>(accA, accB, h, L < 4 ? L : 4, sbase);  // head slots 0..3
+  if (L > 4) gather2_n<6>(accA, accB, h, L < kHeadSlots ? L - 4 : 2, sbase);  // head slots 4..5
   if (L > kHeadSlots) {
     uint32_t rem = L - kHeadSlots;
     cp += kChunkBytes;
     for (; rem > kChunkSlots; rem -= kChunkSlots) {
       const uint4 nx = lds128(cp);  // next chunk in flight while this one is gathered
       cp += kChunkBytes;
-      gather_xor<0, 8>(acc, c, sbase);
+      gather2<0, 4>(accA, accB, c, sbase);
+      gather2<4, 4>(accA, accB, c, sbase);
       c = nx;
     }
-    gather_xor_n<0>(acc, c, rem, sbase);
+    gather2_n<0>(accA, accB, c, rem < 4 ? rem : 4, sbase);
+    if (rem > 4) gather2_n<4>(accA, accB, c, rem - 4, sbase);
   }
   const bool wsplit = ctrl & kSplitBit;
-  if (wsplit) {  // warp-split row: combine the eight half-groups' partial XORs (all lanes get it)
+  // the lane's 32 B in byte order: accA holds piece 2*l2 + (g&1), accB the other
+  const bool sg = grp & 1;
+  uint4 lo = sg ? accB : accA, hi = sg ? accA : accB;
+  if (wsplit) {  // warp-split row: combine the sixteen groups' partial XORs (all lanes get it)
 #pragma unroll
-    for (int o = 4; o <= 16; o <<= 1) {
-      acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, o);
-      acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, o);
-      acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, o);
-      acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, o);
+    for (int o = 2; o <= 16; o <<= 1) {
+      shfl_xor_into(lo, o);
+      shfl_xor_into(hi, o);
     }
-  } else if (ctrl & kPairSplitBit) {  // pair-split groups: both halves take the partner's part
-    uint4 o;
-    o.x = __shfl_xor_sync(0xffffffffu, acc.x, 4);
-    o.y = __shfl_xor_sync(0xffffffffu, acc.y, 4);
-    o.z = __shfl_xor_sync(0xffffffffu, acc.z, 4);
-    o.w = __shfl_xor_sync(0xffffffffu, acc.w, 4);
-    if (h.y & kPairFlag) xor_into(acc, o);
+  } else if (ctrl & kPairSplitBit) {  // pair-split: both halves (groups g, g^2) take the other's part
+    uint4 oa, ob;
+    oa.x = __shfl_xor_sync(0xffffffffu, lo.x, 4);
+    oa.y = __shfl_xor_sync(0xffffffffu, lo.y, 4);
+    oa.z = __shfl_xor_sync(0xffffffffu, lo.z, 4);
+    oa.w = __shfl_xor_sync(0xffffffffu, lo.w, 4);
+    ob.x = __shfl_xor_sync(0xffffffffu, hi.x, 4);
+    ob.y = __shfl_xor_sync(0xffffffffu, hi.y, 4);
+    ob.z = __shfl_xor_sync(0xffffffffu, hi.z, 4);
+    ob.w = __shfl_xor_sync(0xffffffffu, hi.w, 4);
+    if (h.y & kPairFlag) {
+      xor_into(lo, oa);
+      xor_into(hi, ob);
+    }
   }
   if (kMode == 0) {
     if (wsplit) {
-      if (half_id == 0) st_stream(row_addr(out1, row, t), acc);
+      if (grp == 0) st_stream32(row_addr(out1, row, t), lo, hi, st256);
     } else if (row != kNoRow) {
-      st_stream(row_addr(out1, row, t), acc);
+      st_stream32(row_addr(out1, row, t), lo, hi, st256);
     }
   } else if (kMode == 1) {
-    tmem_st16(tcol, acc);
+    tmem_st32(tcol, lo, hi);
   } else {
-    const uint4 prev = tmem_ld16(tcol);                                   // own row, slice s
-    const uint32_t own = __shfl_xor_sync(0xffffffffu, row, 4);            // R_h (row = R_{h^1})
-    const bool hi = half_id & 1;
-    const uint32_t ra = hi ? row : own, rb = hi ? own : row;              // R_{2q}, R_{2q+1}
-    // out1 / out2 = this lane's 16 B in the pair's line at the half it writes of R_{2q} / R_{2q+1}
-    // (per tile: even half-groups the first tile's half of R_{2q}, odd ones the second's, and the
-    // other way round for R_{2q+1})
-    // line of R_{2q}: even half-group its first-tile half (TMEM), odd half-group the second (computed)
-    if (ra != kNoRow && (!wsplit || half_id < 2)) st_stream(row_addr(out1, ra, t), hi ? acc : prev);
-    // line of R_{2q+1}: even half-group the second-tile half (computed), odd half-group its first (TMEM)
-    if (rb != kNoRow && !wsplit) st_stream(row_addr(out2, rb, t), hi ? prev : acc);
+    uint4 plo, phi;
+    tmem_ld32(tcol, plo, phi);                                            // own row, slice s
+    const uint32_t own = __shfl_xor_sync(0xffffffffu, row, 2);            // R_g (row = R_{g^1})
+    const bool odd = grp & 1;
+    const uint32_t ra = odd ? row : own, rb = odd ? own : row;            // R_{2q}, R_{2q+1}
+    // out1 / out2 = this lane's 32 B in the pair's line at the half it writes of R_{2q} / R_{2q+1}
+    // line of R_{2q}: even group its first-tile half (TMEM), odd group the second (computed)
+    if (ra != kNoRow && (!wsplit || grp < 2)) st_stream32(row_addr(out1, ra, t), odd ? lo : plo, odd ? hi : phi, st256);
+    // line of R_{2q+1}: even group the second-tile half (computed), odd group its first (TMEM)
+    if (rb != kNoRow && !wsplit) st_stream32(row_addr(out2, rb, t), odd ? plo : lo, odd ? phi : hi, st256);
   }
 }
 
@@ -345,6 +394,10 @@ __device__ __forceinline__ bool tile_of(const SmemArgs &a, uint32_t i, uint32_t 
 //     TMEM-parked halves and full 128-B lines paired).
 // Buffers alternate (tile i uses buffer i&1), so tile i+1 streams in while tile i computes, and a
 // consumer warp that finishes tile i early starts tile i+1 without waiting for the others.
+// kSt256: the caller's coded rows are 32-B aligned (base and stride), so every lane's 32 B leave in
+// one 256-bit store (else two 128-bit ones; a compile-time choice: a runtime flag tested per store
+// cost 2.5% on config 4)
+template <bool kSt256>
 __global__ void __launch_bounds__(kThreads, 1)
     fsb_smem_encode(const __grid_constant__ CUtensorMap tmap, const SmemArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -515,16 +568,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ------------------------------------------------------------------- consumer warps
-  const uint32_t half_id = lane >> 2, lane4 = lane & 3;
+  const uint32_t grp = lane >> 1, l2 = lane & 1;  // group (2 lanes, 32 B each, of a 64-B row slice)
   const uint32_t nitems = __ldg(&a.warp_info[warp * 3 + 0]);
   const uint32_t head_b = smem_u32(sched_s) + __ldg(&a.warp_info[warp * 3 + 1]) * kChunkBytes;
   const uint32_t cont_b = smem_u32(sched_s) + (a.cont_base + __ldg(&a.warp_info[warp * 3 + 2])) * kChunkBytes;
   // TMEM: this warp's lane quarter (warp % 4) and its column block after the earlier warps of the
-  // same quarter (4 columns = 16 B per lane per item)
+  // same quarter (8 columns = 32 B per lane per item)
   uint32_t tcol0 = 0;
   if (a.paired) {
     uint32_t col = 0;
-    for (int w = warp & 3; w < warp; w += 4) col += 4 * __ldg(&a.warp_info[w * 3 + 0]);
+    for (int w = warp & 3; w < warp; w += 4) col += 8 * __ldg(&a.warp_info[w * 3 + 0]);
     tcol0 = *tmem_slot + ((32u * (warp & 3)) << 16) + col;
   }
   const long long t_start = (a.debug & 2) ? clock64() : 0;
@@ -533,9 +586,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t b = i & 1, ph = (i >> 1) & 1;
     const int mode = (a.paired && i < a.pair_tiles) ? 1 + (i & 1) : 0;
     const uint32_t first = (blockIdx.x & 1) ? kSliceBytes : 0;  // line offset of the pair's first tile
-    // odd tiles of a pair read the partner half-group's schedule (its rows, their slice s+1)
-    const uint32_t hsel = (mode == 2 ? half_id ^ 1 : half_id) * 16;
-    const uint32_t sbase = smem_base + b * buf_bytes + lane4 * 16;  // this lane's 16 B of tile row 0
+    // odd tiles of a pair read the partner group's schedule (its rows, their slice s+1)
+    const uint32_t hsel = (mode == 2 ? grp ^ 1 : grp) * 16;
+    // this lane's first piece of tile row 0 (32 B per lane; pieces ordered by the bank rule)
+    const uint32_t sbase = smem_base + b * buf_bytes + l2 * 32 + (grp & 1) * 16;
     uint32_t hp = head_b + hsel, cp = cont_b + hsel;
     uint4 h0 = lds128(hp);
     long long t_wait0 = 0;
@@ -555,10 +609,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // half this lane writes of R_{2q} (out1) and of R_{2q+1} (out2) -- `first` = byte offset in the
     // line of the pair's first tile
     uint8_t *out1 = a.coded + stripe * a.coded_stride +
-                    static_cast<uint64_t>(mode ? (slice & ~1u) : slice) * kSliceBytes + lane4 * 16;
+                    static_cast<uint64_t>(mode ? (slice & ~1u) : slice) * kSliceBytes + l2 * 32;
     uint8_t *out2 = out1;
     if (mode) {
-      const bool hi = half_id & 1;
+      const bool hi = grp & 1;
       out1 += hi ? kSliceBytes - first : first;
       out2 += hi ? first : kSliceBytes - first;
     }
@@ -566,11 +620,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // items, with the next head chunk in flight (2-way unrolled so no register moves)
     for (uint32_t it = 0; it < nitems; it += 2) {
       const uint4 h1 = lds128(hp + kChunkBytes);
-      lt_item(h0, cp, sbase, out1, out2, t32, half_id, tcol0 + 4 * it, mode);
+      lt_item(h0, cp, sbase, out1, out2, t32, grp, tcol0 + 8 * it, mode, kSt256);
       if (it + 1 >= nitems) break;
       h0 = lds128(hp + 2 * kChunkBytes);
       hp += 2 * kChunkBytes;
-      lt_item(h1, cp, sbase, out1, out2, t32, half_id, tcol0 + 4 * (it + 1), mode);
+      lt_item(h1, cp, sbase, out1, out2, t32, grp, tcol0 + 8 * (it + 1), mode, kSt256);
     }
     if (mode == 1) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // parked before reuse
     __syncwarp();
@@ -1217,8 +1271,11 @@ fs_status upload_graph(Graph &g) {
       if ((st = upload(&g.dev.warp_info, g.sched.warp_info.data(), g.sched.warp_info.size())) != FS_OK) return st;
       if ((st = upload(&g.dev.pre_slots, g.sched.pre_slots.data(), g.sched.pre_slots.size())) != FS_OK) return st;
       if ((st = upload(&g.dev.pre_level_ptr, g.pre_level_ptr.data(), g.pre_level_ptr.size())) != FS_OK) return st;
-      e = cudaFuncSetAttribute(fsb_smem_encode, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(fsb_smem_encode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(g.smem_bytes));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fsb_smem_encode<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(g.smem_bytes));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     }
   }
@@ -1325,7 +1382,7 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
       uint32_t need = 0;
       for (int q = 0; q < 4; ++q) {
         uint32_t c = 0;
-        for (int w = q; w < static_cast<int>(g.sched.nconsumer); w += 4) c += 4 * g.sched.warp_info[w * 3 + 0];
+        for (int w = q; w < static_cast<int>(g.sched.nconsumer); w += 4) c += 8 * g.sched.warp_info[w * 3 + 0];
         need = std::max(need, c);
       }
       uint32_t cols = 32;
@@ -1384,7 +1441,9 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = attr;
     lc.numAttrs = pdl_enabled() ? 1 : 0;  // the prologue may overlap the previous grid's tail
-    e = cudaLaunchKernelEx(&lc, fsb_smem_encode, tmap, a);
+    const bool st256 = reinterpret_cast<uintptr_t>(coded) % 32 == 0 && coded_stride % 32 == 0;
+    e = st256 ? cudaLaunchKernelEx(&lc, fsb_smem_encode<true>, tmap, a)
+              : cudaLaunchKernelEx(&lc, fsb_smem_encode<false>, tmap, a);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "fsb_smem_encode launch");
     *launches = 1;
