@@ -397,7 +397,11 @@ __device__ __forceinline__ bool tile_of(const SmemArgs &a, uint32_t i, uint32_t 
 // kSt256: the caller's coded rows are 32-B aligned (base and stride), so every lane's 32 B leave in
 // one 256-bit store (else two 128-bit ones; a compile-time choice: a runtime flag tested per store
 // cost 2.5% on config 4)
-template <bool kSt256>
+// kTmemHeads (paired launches whose TMEM columns allow it): every item's head chunk -- the lane's
+// own group's 16 B and its partner group's -- is copied into tensor memory once per CTA and read
+// from there with tcgen05.ld, off the shared-memory port (the continuation chunks stay in shared
+// memory).
+template <bool kSt256, bool kTmemHeads>
 __global__ void __launch_bounds__(kThreads, 1)
     fsb_smem_encode(const __grid_constant__ CUtensorMap tmap, const SmemArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -573,12 +577,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t head_b = smem_u32(sched_s) + __ldg(&a.warp_info[warp * 3 + 1]) * kChunkBytes;
   const uint32_t cont_b = smem_u32(sched_s) + (a.cont_base + __ldg(&a.warp_info[warp * 3 + 2])) * kChunkBytes;
   // TMEM: this warp's lane quarter (warp % 4) and its column block after the earlier warps of the
-  // same quarter (8 columns = 32 B per lane per item)
-  uint32_t tcol0 = 0;
+  // same quarter: 8 columns (32 B per lane) per item for the parked results, then (kTmemHeads) 8
+  // per item for the head chunks (own group's 16 B, partner group's 16 B)
+  constexpr uint32_t kColsPerItem = kTmemHeads ? 16 : 8;
+  uint32_t tcol0 = 0, hcol0 = 0;
   if (a.paired) {
     uint32_t col = 0;
-    for (int w = warp & 3; w < warp; w += 4) col += 8 * __ldg(&a.warp_info[w * 3 + 0]);
+    for (int w = warp & 3; w < warp; w += 4) col += kColsPerItem * __ldg(&a.warp_info[w * 3 + 0]);
     tcol0 = *tmem_slot + ((32u * (warp & 3)) << 16) + col;
+    hcol0 = tcol0 + 8 * nitems;
+  }
+  if (kTmemHeads) {
+    for (uint32_t it = 0; it < nitems; ++it) {
+      tmem_st16(hcol0 + 8 * it, lds128(head_b + it * kChunkBytes + grp * 16));
+      tmem_st16(hcol0 + 8 * it + 4, lds128(head_b + it * kChunkBytes + (grp ^ 1) * 16));
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   const long long t_start = (a.debug & 2) ? clock64() : 0;
   uint32_t stripe, slice;
@@ -591,7 +605,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // this lane's first piece of tile row 0 (32 B per lane; pieces ordered by the bank rule)
     const uint32_t sbase = smem_base + b * buf_bytes + l2 * 32 + (grp & 1) * 16;
     uint32_t hp = head_b + hsel, cp = cont_b + hsel;
-    uint4 h0 = lds128(hp);
+    uint4 h0 = make_uint4(0, 0, 0, 0);
+    if (!kTmemHeads) h0 = lds128(hp);
     long long t_wait0 = 0;
     if (a.debug & 2) t_wait0 = clock64();
     if (a.wait_ns) mbar_wait_backoff(smem_u32(&ready[b]), ph, a.wait_ns);
@@ -617,14 +632,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       out2 += hi ? first : kSliceBytes - first;
     }
     const uint32_t t32 = static_cast<uint32_t>(a.t);
-    // items, with the next head chunk in flight (2-way unrolled so no register moves)
-    for (uint32_t it = 0; it < nitems; it += 2) {
-      const uint4 h1 = lds128(hp + kChunkBytes);
-      lt_item(h0, cp, sbase, out1, out2, t32, grp, tcol0 + 8 * it, mode, kSt256);
-      if (it + 1 >= nitems) break;
-      h0 = lds128(hp + 2 * kChunkBytes);
-      hp += 2 * kChunkBytes;
-      lt_item(h1, cp, sbase, out1, out2, t32, grp, tcol0 + 8 * (it + 1), mode, kSt256);
+    if (kTmemHeads) {
+      const uint32_t hc = hcol0 + (mode == 2 ? 4 : 0);
+      for (uint32_t it = 0; it < nitems; ++it)
+        lt_item(tmem_ld16(hc + 8 * it), cp, sbase, out1, out2, t32, grp, tcol0 + 8 * it, mode, kSt256);
+    } else {
+      // items, with the next head chunk in flight (2-way unrolled so no register moves)
+      for (uint32_t it = 0; it < nitems; it += 2) {
+        const uint4 h1 = lds128(hp + kChunkBytes);
+        lt_item(h0, cp, sbase, out1, out2, t32, grp, tcol0 + 8 * it, mode, kSt256);
+        if (it + 1 >= nitems) break;
+        h0 = lds128(hp + 2 * kChunkBytes);
+        hp += 2 * kChunkBytes;
+        lt_item(h1, cp, sbase, out1, out2, t32, grp, tcol0 + 8 * (it + 1), mode, kSt256);
+      }
     }
     if (mode == 1) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // parked before reuse
     __syncwarp();
@@ -1271,11 +1292,14 @@ fs_status upload_graph(Graph &g) {
       if ((st = upload(&g.dev.warp_info, g.sched.warp_info.data(), g.sched.warp_info.size())) != FS_OK) return st;
       if ((st = upload(&g.dev.pre_slots, g.sched.pre_slots.data(), g.sched.pre_slots.size())) != FS_OK) return st;
       if ((st = upload(&g.dev.pre_level_ptr, g.pre_level_ptr.data(), g.pre_level_ptr.size())) != FS_OK) return st;
-      e = cudaFuncSetAttribute(fsb_smem_encode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(g.smem_bytes));
+      const int sb = static_cast<int>(g.smem_bytes);
+      e = cudaFuncSetAttribute(fsb_smem_encode<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
       if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(fsb_smem_encode<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(g.smem_bytes));
+        e = cudaFuncSetAttribute(fsb_smem_encode<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fsb_smem_encode<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fsb_smem_encode<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     }
   }
@@ -1374,9 +1398,16 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     a.sched_chunks = static_cast<uint32_t>(g.sched.words.size() / (kChunkBytes / 4));
     // paired tiles (adjacent 64-B slices of a stripe back to back, rows leave as full 128-B lines
     // via TMEM): even slice count and start, and the warps' TMEM column blocks fit one lane quarter
+    bool tmem_heads = false;
     {
       static const int paired_env = [] {
         const char *e = std::getenv("FSB_PAIRED");
+        return e ? std::atoi(e) : 1;
+      }();
+      // TMEM columns per lane quarter: 8 per item for the parked results, 8 more per item when the
+      // head chunks fit there too (FSB_TMEM_HEADS=0: never, tuning)
+      static const int heads_env = [] {
+        const char *e = std::getenv("FSB_TMEM_HEADS");
         return e ? std::atoi(e) : 1;
       }();
       uint32_t need = 0;
@@ -1385,6 +1416,8 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
         for (int w = q; w < static_cast<int>(g.sched.nconsumer); w += 4) c += 8 * g.sched.warp_info[w * 3 + 0];
         need = std::max(need, c);
       }
+      tmem_heads = heads_env && 2 * need <= 512;
+      if (tmem_heads) need *= 2;
       uint32_t cols = 32;
       while (cols < need) cols <<= 1;
       // ... and only when there are more tiles than SMs: a call of at most one tile per SM
@@ -1442,8 +1475,13 @@ fs_status launch_encode(const Graph &g, uint32_t S, const uint8_t *data, uint64_
     lc.attrs = attr;
     lc.numAttrs = pdl_enabled() ? 1 : 0;  // the prologue may overlap the previous grid's tail
     const bool st256 = reinterpret_cast<uintptr_t>(coded) % 32 == 0 && coded_stride % 32 == 0;
-    e = st256 ? cudaLaunchKernelEx(&lc, fsb_smem_encode<true>, tmap, a)
-              : cudaLaunchKernelEx(&lc, fsb_smem_encode<false>, tmap, a);
+    tmem_heads = tmem_heads && a.paired;
+    if (st256)
+      e = tmem_heads ? cudaLaunchKernelEx(&lc, fsb_smem_encode<true, true>, tmap, a)
+                     : cudaLaunchKernelEx(&lc, fsb_smem_encode<true, false>, tmap, a);
+    else
+      e = tmem_heads ? cudaLaunchKernelEx(&lc, fsb_smem_encode<false, true>, tmap, a)
+                     : cudaLaunchKernelEx(&lc, fsb_smem_encode<false, false>, tmap, a);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "fsb_smem_encode launch");
     *launches = 1;
