@@ -583,6 +583,23 @@ def test_smem_pair_rounds_with_tail_singles(S):
     _assert_equal(y, Y, "coded S=%d" % S)
 
 
+@pytest.mark.parametrize("env", [{"FSB_TMEM_HEADS": "0"}, {"FSB_ITEM_OVERHEAD": "3", "FSB_SPLIT1": "40",
+                                                            "FSB_SPLIT2": "80"}])
+def test_smem_schedule_variants_by_env(env):
+    """The SMEM kernel's other schedule / layout choices (read once per process, so each runs in a
+    fresh process): item heads in shared memory instead of TMEM on a paired launch
+    (FSB_TMEM_HEADS=0), and another split-threshold / LPT setting (more pair- and warp-splits) --
+    config 4 (256 stripes) in full against the oracle, SMEM variant."""
+    _need_gpu()
+    import subprocess
+    import sys as _sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([_sys.executable, os.path.join(root, "tools", "gpu", "check_cfg.py"), "4", "smem"],
+                       capture_output=True, text=True, env=dict(os.environ, **env), timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().endswith("ok"), r.stdout
+
+
 @pytest.mark.parametrize("band_cfg", ["0", "1", "2", "4"])
 def test_band_kernel_instances_by_env(band_cfg):
     """The other GLOBAL band-kernel instances FSB_BAND_CFG selects (read once per process, so each
