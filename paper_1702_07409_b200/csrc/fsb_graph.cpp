@@ -485,6 +485,16 @@ void build_smem_schedule(Graph &g) {
   // within a degree class d, a row with x even sources pairs best with one with d - x (its odds
   // then meet the partner's evens one for one): exact complements first, then the extremes of
   // what is left
+  // The rows left after the exact complements of every class are matched across classes (greedy,
+  // least parity padding; FSB_PAIR_GLOBAL=0: extremes within the class, the earlier rule).  Same
+  // box (profiles/r02_s4c/ab_pair_global.txt): config 6 0.6838 -> 0.6757 ms, config 7 0.6313 ->
+  // 0.6289, config 4 unchanged (its parity padding falls 498 -> 432 slots per tile, its length
+  // padding rises 482 -> 548).
+  static const int pair_global = [] {
+    const char *e = std::getenv("FSB_PAIR_GLOBAL");
+    return e ? std::atoi(e) : 1;
+  }();
+  std::vector<uint32_t> pool;
   uint32_t carry = UINT32_MAX;  // an unpaired row left over from the previous class
   for (size_t c0 = 0; c0 < light.size();) {
     size_t c1 = c0;
@@ -513,6 +523,11 @@ void build_smem_schedule(Graph &g) {
     std::vector<uint32_t> cls;
     if (carry != UINT32_MAX) cls.push_back(carry), carry = UINT32_MAX;
     for (uint32_t x = 0; x <= d; ++x) cls.insert(cls.end(), by_x[x].begin(), by_x[x].end());
+    if (pair_global) {
+      pool.insert(pool.end(), cls.begin(), cls.end());
+      c0 = c1;
+      continue;
+    }
     std::stable_sort(cls.begin(), cls.end(), [&](uint32_t a, uint32_t b) { return ecount[a] < ecount[b]; });
     size_t lo = 0, hi = cls.size();
     while (hi - lo >= 2) {
@@ -524,6 +539,32 @@ void build_smem_schedule(Graph &g) {
     c0 = c1;
   }
   if (carry != UINT32_MAX) pairs.push_back(make_pair(carry, UINT32_MAX));
+  if (!pool.empty()) {
+    // greedy: heaviest leftover first, its partner the unpaired leftover with the least parity
+    // padding 2 (max(eA, oB) + max(oA, eB)) - dA - dB, ties to the closest degree
+    std::stable_sort(pool.begin(), pool.end(), [&](uint32_t a, uint32_t b) { return degree(a) > degree(b); });
+    std::vector<char> used(pool.size(), 0);
+    for (size_t i = 0; i < pool.size(); ++i) {
+      if (used[i]) continue;
+      used[i] = 1;
+      const uint32_t a = pool[i], da = degree(a), ea = ecount[a], oa = da - ea;
+      size_t best = SIZE_MAX;
+      int64_t bcost = INT64_MAX;
+      for (size_t j = i + 1; j < pool.size(); ++j) {
+        if (used[j]) continue;
+        const uint32_t b = pool[j], db = degree(b), eb = ecount[b], ob = db - eb;
+        const int64_t pad = 2 * static_cast<int64_t>(std::max(ea, ob) + std::max(oa, eb)) - da - db;
+        const int64_t cost = pad * 4096 + (static_cast<int64_t>(da) - db);
+        if (cost < bcost) bcost = cost, best = j;
+      }
+      if (best == SIZE_MAX) {
+        pairs.push_back(make_pair(a, UINT32_MAX));
+      } else {
+        used[best] = 1;
+        pairs.push_back(make_pair(a, pool[best]));
+      }
+    }
+  }
   std::stable_sort(pairs.begin(), pairs.end(),
                    [](const Pair &a, const Pair &b) { return a.seq[0].size() > b.seq[0].size(); });
   for (size_t i = 0; i < pairs.size(); i += kPairsPerItem) {
