@@ -584,11 +584,12 @@ def test_smem_pair_rounds_with_tail_singles(S):
 
 
 @pytest.mark.parametrize("env", [{"FSB_TMEM_HEADS": "0"}, {"FSB_ITEM_OVERHEAD": "3", "FSB_SPLIT1": "40",
-                                                            "FSB_SPLIT2": "80"}])
+                                                            "FSB_SPLIT2": "80"}, {"FSB_PAIR_GLOBAL": "0"}])
 def test_smem_schedule_variants_by_env(env):
     """The SMEM kernel's other schedule / layout choices (read once per process, so each runs in a
     fresh process): item heads in shared memory instead of TMEM on a paired launch
-    (FSB_TMEM_HEADS=0), and another split-threshold / LPT setting (more pair- and warp-splits) --
+    (FSB_TMEM_HEADS=0), another split-threshold / LPT setting (more pair- and warp-splits), and the
+    within-class pairing of leftover rows (FSB_PAIR_GLOBAL=0) --
     config 4 (256 stripes) in full against the oracle, SMEM variant."""
     _need_gpu()
     import subprocess
