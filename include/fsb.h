@@ -205,14 +205,16 @@ FSB_API fs_status fs_encode_host(const fs_graph *g, uint32_t num_stripes,
 
 /* Diagnostic view of the SMEM kernel's host-built LT schedule (owned by g):
  * words[nwords] = two chunk streams of uint32 words, the heads stream first and the conts stream
- * from chunk cont_base on (chunk c = words 32c..32c+31; half-group h's 4 words at 32c+4h; half-
- * group h = lanes 4h..4h+3 of a warp, h = 2*group + half).  warp_info[16*3] = {items, first head
- * chunk, first cont chunk} per consumer warp (nwarps of them).  A slot is an 11-bit tile row (data m -> m, check i
- * -> kpad+i, padding -> zero_even or zero_even+1); a slot word packs two slots as a | b << 21.
- * An item's head chunk holds, per half-group, word 0 = row | ctrl << 16 (ctrl = L | split << 15;
- * row 0xFFFF = no output) and slots 0..5 in words 1..3; slots 6..L-1 follow in the conts stream,
- * 8 per chunk.  In every step, half 0 of a group reads an even row iff half 1 reads an odd one
- * (shared-memory bank rule).  FS_EUNSUPPORTED when the graph is not SMEM-eligible.          */
+ * from chunk cont_base on (chunk c = words 64c..64c+63; group g's 4 words at 64c+4g; group g =
+ * lanes 2g, 2g+1 of a warp, 32 B each of a 64-B row slice; pair q, half h sits in group
+ * 4(q>>1) + (q&1) + 2h).  warp_info[nwarps*3] = {items, first head chunk, first cont chunk} per
+ * consumer warp.  A slot is an 11-bit tile row (data m -> m, check i -> kpad+i, padding ->
+ * zero_even or zero_even+1); a slot word packs two slots as a | b << 21.  An item's head chunk
+ * holds, per group, word 0 = row | ctrl << 16 (ctrl = L | pair-split << 14 | warp-split << 15;
+ * row 0xFFFF = no output) and slots 0..5 in words 1..3 (word 1 bit 11: the group's pair is a
+ * pair-split); slots 6..L-1 follow in the conts stream, 8 per chunk.  In every step groups g and
+ * g^2 read rows of opposite parity (shared-memory bank rule).  FS_EUNSUPPORTED when the graph is
+ * not SMEM-eligible.                                                                         */
 /* The fixed-size LT edge windows of the GLOBAL window kernel (host views, owned by g): window w
  * (w < *count) covers the LT rows [hdr[2w], hdr[2w+2]) (the last window ends at n); hdr[2w+1] =
  * its batches of 4 edges; its *entries edge slots ent[w * *entries ...] hold the rows' column
