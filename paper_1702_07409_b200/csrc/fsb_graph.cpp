@@ -541,7 +541,9 @@ void build_smem_schedule(Graph &g) {
   if (carry != UINT32_MAX) pairs.push_back(make_pair(carry, UINT32_MAX));
   if (!pool.empty()) {
     // greedy: heaviest leftover first, its partner the unpaired leftover with the least parity
-    // padding 2 (max(eA, oB) + max(oA, eB)) - dA - dB, ties to the closest degree
+    // padding 2 (max(eA, oB) + max(oA, eB)) - dA - dB, ties to the closest degree; the scan looks
+    // at the next kScan unpaired rows in degree order (a pool of n rows costs O(n kScan), not n^2)
+    constexpr size_t kScan = 512;
     std::stable_sort(pool.begin(), pool.end(), [&](uint32_t a, uint32_t b) { return degree(a) > degree(b); });
     std::vector<char> used(pool.size(), 0);
     for (size_t i = 0; i < pool.size(); ++i) {
@@ -550,8 +552,10 @@ void build_smem_schedule(Graph &g) {
       const uint32_t a = pool[i], da = degree(a), ea = ecount[a], oa = da - ea;
       size_t best = SIZE_MAX;
       int64_t bcost = INT64_MAX;
-      for (size_t j = i + 1; j < pool.size(); ++j) {
+      size_t seen = 0;
+      for (size_t j = i + 1; j < pool.size() && seen < kScan; ++j) {
         if (used[j]) continue;
+        ++seen;
         const uint32_t b = pool[j], db = degree(b), eb = ecount[b], ob = db - eb;
         const int64_t pad = 2 * static_cast<int64_t>(std::max(ea, ob) + std::max(oa, eb)) - da - db;
         const int64_t cost = pad * 4096 + (static_cast<int64_t>(da) - db);
