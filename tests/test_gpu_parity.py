@@ -200,6 +200,10 @@ EDGE_CASES = [
                                        rsd_delta=0.01, seed=17), 400),
     ("p_over_64_checks", dict(k=500, p=150, d_p=5, n=600, t=128, dist=configs.RSD, rsd_c=0.1,
                               rsd_delta=0.05, seed=18), 320),
+    # every row of degree 1 on one even source: no even/odd complements at all, so all 20,000 rows
+    # go through the cross-class leftover matching (bounded scan) of the SMEM schedule
+    ("k1_many_rows", dict(k=1, p=0, d_p=0, n=20000, t=256, dist=configs.FINITE, seed=19,
+                          fin_deg=configs.OMEGA_DEGREES, fin_prob=configs.OMEGA_PROBS), 3),
 ]
 
 
